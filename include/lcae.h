@@ -1,0 +1,150 @@
+/*
+ * lcae.h — C ABI of liblcae.so: one training step of a locally-connected (untied-weight)
+ * RICA sparse-autoencoder layer on one B200 (sm_100a).
+ *
+ * The operation (§3.1 eq. "RICA", read as DESIGN.md "Readings" R1-R11):
+ * for every receptive field f of the layer (row-major grid) and every
+ * sample x^(i) of the batch (patch x_f^(i) flattened in (ry, rx, c) order):
+ *
+ *     h    = alpha_f W_f x                                   (encode, "alpha W x")
+ *     s_G  = sqrt(eps + sum_{j in G} h_j^2)                   (L2 pooling, groups of g filters; g=1: the
+ *                                                              paper's lambda sqrt((alpha W x)^2))
+ *     r    = W_f^T h + b_f,  e = r - x                         (decode with offset b)
+ *     J   += ||e||^2 + lambda sum_G s_G                        (reconstruction + sparsity, summed; R6)
+ *     dW_f, dalpha_f, db_f, dX (overlap-added over fields)     (exact gradients of J; R11)
+ *     W_f <- rownorm(W_f - lr dW_f) (optional momentum); alpha_f <- max(alpha_f - lr dalpha_f, alpha_min);
+ *     b_f <- b_f - lr db_f                                     (projected SGD)
+ *
+ * Precision: LCAE_FP32 computes every product and sum in fp32 (FFMA, no TF32) with an fp64 loss sum;
+ * LCAE_BF16 feeds bf16 operands (x, W, h, delta, D rounded RN-even) to tcgen05 tensor cores with fp32
+ * accumulation (TMEM), fp32 epilogues and fp32 master weights.
+ *
+ * Conventions
+ *  - All functions return lcae_status; on error, lcae_last_error() (thread-local, library-owned
+ *    string) says why. Status codes 2/3/4 mirror SPEC.md:531's exit codes (config/data/numeric).
+ *  - Data pointers marked "host or device" may be either: the library inspects them with
+ *    cudaPointerGetAttributes and copies host data through its own device staging buffers on the
+ *    layer's stream. Device pointers must be on the layer's device.
+ *  - Everything is ordered on cfg.stream (a cudaStream_t; NULL = legacy default stream). Calls whose
+ *    outputs are host memory or that return a host scalar (loss != NULL) synchronise that stream.
+ *  - A layer handle is not thread-safe; one handle per host thread.
+ *  - The library owns all device memory it allocates; nothing is freed by the caller.
+ *
+ * Layouts (canonical, exchanged with callers and the test oracle)
+ *  - image x / dx: NHWC float32 [m][img_h][img_w][img_c].
+ *  - W: float32 [F][k][n], n = (ry*rf_w + rx)*img_c + c; alpha: float32 [F]; b: float32 [F][n].
+ *  - pooled p: float32 [m][grid_r][grid_c][k/g] (p = s_G, the L2-pooled code).
+ *  - F = grid_r*grid_c fields in row-major order over THIS layer's image (a rank of a model-parallel
+ *    run passes its extended input region — owned pixels plus halo — as its image; global field ids
+ *    are field_row0/field_col0/global_grid_c offsets, used only by the degenerate-row generator).
+ */
+#ifndef LCAE_H_
+#define LCAE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lcae_layer lcae_layer; /* opaque; owns all its device memory */
+
+typedef enum {
+  LCAE_OK = 0,
+  LCAE_ERR_CONFIG = 2,  /* geometry / pooling / precision / size not supported */
+  LCAE_ERR_DATA = 3,    /* bad data pointer, shape or non-finite input */
+  LCAE_ERR_NUMERIC = 4, /* non-finite loss ("numeric error") */
+  LCAE_ERR_CUDA = 5,    /* CUDA runtime / driver failure (message has the CUDA error string) */
+  LCAE_ERR_ARG = 7      /* NULL handle or NULL required pointer */
+} lcae_status;
+
+typedef enum { LCAE_FP32 = 0, LCAE_BF16 = 1 } lcae_precision;
+
+typedef struct {
+  int32_t img_h, img_w, img_c; /* input image (this rank's extended region) */
+  int32_t rf_h, rf_w, stride;  /* receptive field and stride; (img-rf) % stride == 0 */
+  int32_t filters;             /* k per field (PAPER.md:95 'output size 4x4x24' = 384 for the paper) */
+  int32_t pool_group;          /* g: divides k and 32; g = 1 == the paper (no pooling) */
+  int32_t batch;               /* m: samples per step */
+  float lambda_;               /* sparsity weight (0.1 for layers 1-2) */
+  float eps;                   /* sqrt smoothing, > 0 recommended */
+  float lr;                    /* SGD learning rate */
+  float momentum;              /* 0 = plain SGD (hot path); > 0 allocates velocity buffers */
+  float alpha_init;            /* initial alpha (when params are not set explicitly) */
+  float alpha_min;             /* alpha clamp (1e-8) */
+  uint64_t seed;               /* degenerate-row re-initialisation generator seed */
+  int32_t precision;           /* lcae_precision */
+  int32_t keep_grads;          /* 1: also store dW/dalpha/db of the last step for lcae_get_grads (tests) */
+  int32_t field_row0, field_col0, global_grid_c; /* global id of local field (r,c) = (row0+r)*ggc + col0+c */
+  void *stream;                /* cudaStream_t; NULL = default stream */
+} lcae_config;
+
+/* Fill *cfg with the defaults of DESIGN.md (lambda 0.1, eps 1e-6, lr 1e-3, momentum 0, alpha 1, 1e-8). */
+void lcae_config_default(lcae_config *cfg);
+
+/* Validate cfg and report the derived geometry without allocating anything.
+ * grid_r/grid_c/n_params may be NULL. n_params = F*(k*n + n + 1).
+ * Errors: LCAE_ERR_CONFIG with the residue for non-divisible extents, g not dividing k
+ * or 32, rf larger than the image, non-positive sizes, unknown precision. */
+lcae_status lcae_geometry(const lcae_config *cfg, int32_t *grid_r, int32_t *grid_c, int64_t *n_params);
+
+/* Create a layer on the current CUDA device: validates cfg (as lcae_geometry), allocates parameters,
+ * gradient/optimizer state and scratch, and initialises W to unit rows from a counter-based generator,
+ * alpha = alpha_init, b = 0 (callers normally overwrite them with lcae_set_params).
+ * *out receives the handle. Errors: CONFIG, CUDA (e.g. out of memory), ARG. */
+lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out);
+
+/* Release everything the handle owns. NULL-safe. Synchronises the layer's stream first. */
+lcae_status lcae_destroy(lcae_layer *L);
+
+/* Copy parameters in (canonical layouts above; host or device pointers). W rows are used as given
+ * (callers pass unit rows). Any pointer may be NULL to leave that tensor unchanged. */
+lcae_status lcae_set_params(lcae_layer *L, const float *W, const float *alpha, const float *b);
+
+/* Copy the current parameters out (host or device pointers; NULL skips). */
+lcae_status lcae_get_params(lcae_layer *L, float *W, float *alpha, float *b);
+
+/* Gradients of the most recent lcae_step, taken at the pre-update parameters (requires keep_grads=1,
+ * else LCAE_ERR_CONFIG). dW [F][k][n], dalpha [F], db [F][n]; host or device; NULL skips. */
+lcae_status lcae_get_grads(lcae_layer *L, float *dW, float *dalpha, float *db);
+
+/* Forward only: pooled code p (nullable) and loss J at the current parameters (nullable; if non-NULL the
+ * call synchronises and returns LCAE_ERR_NUMERIC when J is not finite). x: host or device NHWC f32. */
+lcae_status lcae_forward(lcae_layer *L, const float *x, float *pooled, double *loss);
+
+/* One training step on batch x (host or device NHWC f32): loss and gradients at the current parameters,
+ * the input gradient dX overlap-added over fields into dx (nullable: the dX contraction still runs,
+ * the result stays in the layer's device buffer — see lcae_dx_device), then the fused projected-SGD
+ * update. loss (nullable) receives J = J_rec + J_sparse of the pre-update parameters (synchronises).
+ * Errors: ARG, DATA, NUMERIC (non-finite loss, parameters already updated), CUDA. */
+lcae_status lcae_step(lcae_layer *L, const float *x, float *dx, double *loss);
+
+/* Loss split of the last step/forward: J_rec and J_sparse (host doubles; synchronises). */
+lcae_status lcae_last_loss(lcae_layer *L, double *j_rec, double *j_sparse);
+
+/* Device pointer of the layer's dX buffer (NHWC f32, valid after lcae_step until the next call). */
+lcae_status lcae_dx_device(lcae_layer *L, float **dx_dev);
+
+/* Number of steps taken and of degenerate rows re-initialised so far. */
+lcae_status lcae_counters(lcae_layer *L, int64_t *steps, int64_t *reinit_rows);
+
+/* Overlap-add for model-parallel halos ("when a layer's input (or output) field spans
+ * multiple GPUs"): dst[i][y0+y][x0+x][c] += src[i][y][x][c] for i<m, y<rows, x<cols, c<C.
+ * dst is NHWC with row width dst_w, src is dense NHWC [m][rows][cols][C]; both device pointers,
+ * ordered on `stream` (cudaStream_t). */
+lcae_status lcae_region_add(void *stream, float *dst, int32_t dst_h, int32_t dst_w, const float *src,
+                            int32_t m, int32_t rows, int32_t cols, int32_t C, int32_t y0, int32_t x0);
+
+/* Kernel launches issued by the last lcae_step / lcae_forward on this handle (bench accounting). */
+int32_t lcae_last_launch_count(lcae_layer *L);
+
+/* Thread-local description of the last error (never NULL). */
+const char *lcae_last_error(void);
+
+/* Library build string: "lcae <version> sm_100a". */
+const char *lcae_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LCAE_H_ */

@@ -1,0 +1,321 @@
+// api.cu — the extern "C" boundary of liblcae.so (declared and documented in include/lcae.h).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace lcae {
+static thread_local std::string g_err = "no error";
+void set_error(const std::string &msg) { g_err = msg; }
+
+static lcae_status config_error(const std::string &m) {
+  set_error(m);
+  return LCAE_ERR_CONFIG;
+}
+
+// Geometry validation (R7) and derived sizes.
+static lcae_status validate(const lcae_config *c, Geo *out) {
+  if (!c) { set_error("NULL config"); return LCAE_ERR_ARG; }
+  if (c->img_h <= 0 || c->img_w <= 0 || c->img_c <= 0 || c->rf_h <= 0 || c->rf_w <= 0 || c->stride <= 0 ||
+      c->filters <= 0 || c->pool_group <= 0 || c->batch <= 0)
+    return config_error("all sizes must be positive");
+  if (c->rf_h > c->img_h || c->rf_w > c->img_w) return config_error("receptive field larger than image");
+  int ry = (c->img_h - c->rf_h) % c->stride, rx = (c->img_w - c->rf_w) % c->stride;
+  if (ry || rx) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "non-divisible extent: residue rows=%d cols=%d for stride %d", ry, rx, c->stride);
+    return config_error(buf);
+  }
+  if (c->filters % c->pool_group) return config_error("pool_group must divide filters");
+  if (32 % c->pool_group) return config_error("pool_group must divide 32");
+  if (c->precision != LCAE_FP32 && c->precision != LCAE_BF16) return config_error("unknown precision");
+  if (!(c->eps >= 0.f) || !(c->lr >= 0.f) || !(c->momentum >= 0.f && c->momentum < 1.f) || !(c->alpha_min > 0.f))
+    return config_error("eps/lr must be >= 0, momentum in [0,1), alpha_min > 0");
+  Geo g{};
+  g.H = c->img_h; g.W = c->img_w; g.C = c->img_c; g.rf_h = c->rf_h; g.rf_w = c->rf_w; g.s = c->stride;
+  g.k = c->filters; g.g = c->pool_group; g.m = c->batch;
+  g.gr = (g.H - g.rf_h) / g.s + 1;
+  g.gc = (g.W - g.rf_w) / g.s + 1;
+  g.F = g.gr * g.gc;
+  g.n = g.rf_h * g.rf_w * g.C;
+  g.RW = g.rf_w * g.C;
+  g.SY = (int64_t)g.W * g.C * g.m;
+  g.SRC_R = (int64_t)g.s * g.SY;
+  g.SRC_C = (int64_t)g.s * g.C * g.m;
+  if ((int64_t)g.H * g.W * g.C * g.m >= (1ll << 31)) return config_error("image x batch too large (>= 2^31 elements)");
+  if (out) *out = g;
+  return LCAE_OK;
+}
+
+static bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Copy `bytes` between any combination of host/device pointers on the layer stream.
+static lcae_status copy_any(lcae_layer *L, void *dst, const void *src, size_t bytes) {
+  LCAE_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, L->st));
+  return LCAE_OK;
+}
+
+// Make x device-resident (staging host data) and convert to the path's internal HWCN layout.
+static lcae_status stage_input(lcae_layer *L, const float *x) {
+  const Geo &g = L->geo;
+  size_t bytes = (size_t)g.m * g.H * g.W * g.C * 4;
+  const float *xd = x;
+  if (!is_device_ptr(x)) {
+    lcae_status s = copy_any(L, L->x_stage, x, bytes);
+    if (s) return s;
+    xd = L->x_stage;
+  }
+  if (L->cfg.precision == LCAE_FP32) return launch_nhwc_to_hwcn_f32(L, xd, L->xt32);
+  return launch_nhwc_to_hwcn_bf16(L, xd, L->xt16);
+}
+
+static lcae_status read_loss(lcae_layer *L, double *loss) {
+  LCAE_CK(cudaMemcpyAsync(L->loss_host, L->loss_dev, 2 * sizeof(double), cudaMemcpyDeviceToHost, L->st));
+  LCAE_CK(cudaStreamSynchronize(L->st));
+  double J = L->loss_host[0] + L->loss_host[1];
+  if (loss) *loss = J;
+  if (!std::isfinite(J)) {
+    set_error("non-finite loss");
+    return LCAE_ERR_NUMERIC;
+  }
+  return LCAE_OK;
+}
+
+}  // namespace lcae
+
+using namespace lcae;
+
+extern "C" {
+
+void lcae_config_default(lcae_config *c) {
+  if (!c) return;
+  memset(c, 0, sizeof *c);
+  c->lambda_ = 0.1f;
+  c->eps = 1e-6f;
+  c->lr = 1e-3f;
+  c->momentum = 0.f;
+  c->alpha_init = 1.f;
+  c->alpha_min = 1e-8f;
+  c->pool_group = 1;
+  c->precision = LCAE_BF16;
+}
+
+const char *lcae_last_error(void) { return g_err.c_str(); }
+const char *lcae_version(void) { return "lcae 0.1.0 sm_100a"; }
+
+lcae_status lcae_geometry(const lcae_config *cfg, int32_t *grid_r, int32_t *grid_c, int64_t *n_params) {
+  Geo g;
+  lcae_status s = validate(cfg, &g);
+  if (s) return s;
+  if (grid_r) *grid_r = g.gr;
+  if (grid_c) *grid_c = g.gc;
+  if (n_params) *n_params = (int64_t)g.F * ((int64_t)g.k * g.n + g.n + 1);
+  return LCAE_OK;
+}
+
+lcae_status lcae_destroy(lcae_layer *L) {
+  if (!L) return LCAE_OK;
+  if (L->st) cudaStreamSynchronize(L->st);
+  cudaDeviceSynchronize();
+  f32_free(L);
+  tc_free(L);
+  for (void *p : {(void *)L->W, (void *)L->sigma, (void *)L->alpha, (void *)L->b, (void *)L->vW, (void *)L->va,
+                  (void *)L->vb, (void *)L->Wb, (void *)L->x_stage, (void *)L->xt32, (void *)L->xt16,
+                  (void *)L->dxt, (void *)L->dx_nhwc, (void *)L->pooled, (void *)L->gW, (void *)L->galpha,
+                  (void *)L->gb, (void *)L->loss_part, (void *)L->loss_dev, (void *)L->reinit_dev,
+                  (void *)L->rowsq})
+    if (p) cudaFree(p);
+  if (L->loss_host) cudaFreeHost(L->loss_host);
+  delete L;
+  return LCAE_OK;
+}
+
+lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
+  if (!out) { set_error("NULL out"); return LCAE_ERR_ARG; }
+  *out = nullptr;
+  Geo g;
+  lcae_status s = validate(cfg, &g);
+  if (s) return s;
+  lcae_layer *L = new lcae_layer();
+  L->cfg = *cfg;
+  if (L->cfg.global_grid_c <= 0) L->cfg.global_grid_c = g.gc;
+  L->geo = g;
+  L->st = (cudaStream_t)cfg->stream;
+#define FAIL(x)                         \
+  do {                                  \
+    lcae_status s_ = (x);               \
+    if (s_) { lcae_destroy(L); return s_; } \
+  } while (0)
+#define CKF(call)                                                                 \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess) {                                                      \
+      set_error(std::string(#call) + ": " + cudaGetErrorString(e_));              \
+      lcae_destroy(L);                                                            \
+      return LCAE_ERR_CUDA;                                                       \
+    }                                                                             \
+  } while (0)
+  CKF(cudaGetDevice(&L->device));
+  CKF(cudaDeviceGetAttribute(&L->sm_count, cudaDevAttrMultiProcessorCount, L->device));
+  const size_t F = g.F, k = g.k, n = g.n, m = g.m, img = (size_t)g.H * g.W * g.C;
+  CKF(cudaMalloc(&L->W, F * k * n * 4));
+  CKF(cudaMalloc(&L->sigma, F * k * 4));
+  CKF(cudaMalloc(&L->alpha, F * 4));
+  CKF(cudaMalloc(&L->b, F * n * 4));
+  if (cfg->momentum > 0.f) {
+    CKF(cudaMalloc(&L->vW, F * k * n * 4));
+    CKF(cudaMalloc(&L->va, F * 4));
+    CKF(cudaMalloc(&L->vb, F * n * 4));
+    CKF(cudaMemsetAsync(L->vW, 0, F * k * n * 4, L->st));
+    CKF(cudaMemsetAsync(L->va, 0, F * 4, L->st));
+    CKF(cudaMemsetAsync(L->vb, 0, F * n * 4, L->st));
+  }
+  CKF(cudaMalloc(&L->x_stage, m * img * 4));
+  CKF(cudaMalloc(&L->dxt, m * img * 4));
+  CKF(cudaMalloc(&L->dx_nhwc, m * img * 4));
+  CKF(cudaMalloc(&L->pooled, m * F * (k / g.g) * 4));
+  CKF(cudaMalloc(&L->loss_part, F * 2 * sizeof(double)));
+  CKF(cudaMalloc(&L->loss_dev, 2 * sizeof(double)));
+  CKF(cudaMemsetAsync(L->loss_dev, 0, 2 * sizeof(double), L->st));
+  CKF(cudaMalloc(&L->reinit_dev, sizeof(int)));
+  CKF(cudaMemsetAsync(L->reinit_dev, 0, sizeof(int), L->st));
+  CKF(cudaMallocHost(&L->loss_host, 2 * sizeof(double)));
+  if (cfg->keep_grads) {
+    CKF(cudaMalloc(&L->gW, F * k * n * 4));
+    CKF(cudaMalloc(&L->galpha, F * 4));
+    CKF(cudaMalloc(&L->gb, F * n * 4));
+  }
+  if (cfg->precision == LCAE_FP32) {
+    CKF(cudaMalloc(&L->xt32, m * img * 4));
+    FAIL(f32_alloc(L));
+  } else {
+    L->n_al = (int)((n + 7) / 8 * 8);
+    CKF(cudaMalloc(&L->Wb, F * k * (size_t)L->n_al * 2));
+    CKF(cudaMalloc(&L->xt16, m * img * 2));
+    CKF(cudaMalloc(&L->rowsq, F * k * 4));
+    FAIL(tc_alloc(L));
+  }
+  FAIL(launch_init_params(L));
+  FAIL(launch_refresh_shadow(L));
+  CKF(cudaStreamSynchronize(L->st));
+  *out = L;
+  return LCAE_OK;
+#undef FAIL
+#undef CKF
+}
+
+lcae_status lcae_set_params(lcae_layer *L, const float *W, const float *alpha, const float *b) {
+  if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
+  const Geo &g = L->geo;
+  lcae_status s;
+  if (W) {
+    if ((s = copy_any(L, L->W, W, (size_t)g.F * g.k * g.n * 4))) return s;
+    // W is taken as given: sigma = 1 (W~ = W)
+    if ((s = launch_fill(L, L->sigma, (int64_t)g.F * g.k, 1.f))) return s;
+    if ((s = launch_refresh_shadow(L))) return s;
+  }
+  if (alpha && (s = copy_any(L, L->alpha, alpha, (size_t)g.F * 4))) return s;
+  if (b && (s = copy_any(L, L->b, b, (size_t)g.F * g.n * 4))) return s;
+  LCAE_CK(cudaStreamSynchronize(L->st));
+  return LCAE_OK;
+}
+
+lcae_status lcae_get_params(lcae_layer *L, float *W, float *alpha, float *b) {
+  if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
+  const Geo &g = L->geo;
+  lcae_status s;
+  if (W) {
+    size_t bytes = (size_t)g.F * g.k * g.n * 4;
+    if (is_device_ptr(W)) {
+      if ((s = launch_get_W(L, W))) return s;
+    } else {
+      float *tmp = nullptr;
+      LCAE_CK(cudaMallocAsync(&tmp, bytes, L->st));
+      if ((s = launch_get_W(L, tmp))) return s;
+      LCAE_CK(cudaMemcpyAsync(W, tmp, bytes, cudaMemcpyDeviceToHost, L->st));
+      LCAE_CK(cudaFreeAsync(tmp, L->st));
+    }
+  }
+  if (alpha && (s = copy_any(L, alpha, L->alpha, (size_t)g.F * 4))) return s;
+  if (b && (s = copy_any(L, b, L->b, (size_t)g.F * g.n * 4))) return s;
+  LCAE_CK(cudaStreamSynchronize(L->st));
+  return LCAE_OK;
+}
+
+lcae_status lcae_get_grads(lcae_layer *L, float *dW, float *dalpha, float *db) {
+  if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
+  if (!L->cfg.keep_grads) return config_error("lcae_get_grads needs keep_grads = 1");
+  const Geo &g = L->geo;
+  lcae_status s;
+  if (dW && (s = copy_any(L, dW, L->gW, (size_t)g.F * g.k * g.n * 4))) return s;
+  if (dalpha && (s = copy_any(L, dalpha, L->galpha, (size_t)g.F * 4))) return s;
+  if (db && (s = copy_any(L, db, L->gb, (size_t)g.F * g.n * 4))) return s;
+  LCAE_CK(cudaStreamSynchronize(L->st));
+  return LCAE_OK;
+}
+
+static lcae_status run(lcae_layer *L, const float *x, bool update, float *dx, float *pooled, double *loss) {
+  if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
+  if (!x) { set_error("NULL input"); return LCAE_ERR_ARG; }
+  L->launches = 0;
+  const Geo &g = L->geo;
+  lcae_status s;
+  if ((s = stage_input(L, x))) return s;
+  s = (L->cfg.precision == LCAE_FP32) ? f32_step(L, update, pooled != nullptr) : tc_step(L, update, pooled != nullptr);
+  if (s) return s;
+  if ((s = launch_loss_reduce(L))) return s;
+  if (update) {
+    if ((s = launch_hwcn_to_nhwc_f32(L, L->dxt, L->dx_nhwc))) return s;
+    if (dx && (s = copy_any(L, dx, L->dx_nhwc, (size_t)g.m * g.H * g.W * g.C * 4))) return s;
+    L->steps++;
+  }
+  if (pooled && (s = copy_any(L, pooled, L->pooled, (size_t)g.m * g.F * (g.k / g.g) * 4))) return s;
+  if (loss || (dx && !is_device_ptr(dx)) || (pooled && !is_device_ptr(pooled))) {
+    if (loss) return read_loss(L, loss);
+    LCAE_CK(cudaStreamSynchronize(L->st));
+  }
+  return LCAE_OK;
+}
+
+lcae_status lcae_forward(lcae_layer *L, const float *x, float *pooled, double *loss) {
+  return run(L, x, false, nullptr, pooled, loss);
+}
+
+lcae_status lcae_step(lcae_layer *L, const float *x, float *dx, double *loss) {
+  return run(L, x, true, dx, nullptr, loss);
+}
+
+lcae_status lcae_last_loss(lcae_layer *L, double *j_rec, double *j_sparse) {
+  if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
+  LCAE_CK(cudaMemcpyAsync(L->loss_host, L->loss_dev, 2 * sizeof(double), cudaMemcpyDeviceToHost, L->st));
+  LCAE_CK(cudaStreamSynchronize(L->st));
+  if (j_rec) *j_rec = L->loss_host[0];
+  if (j_sparse) *j_sparse = L->loss_host[1];
+  return LCAE_OK;
+}
+
+lcae_status lcae_dx_device(lcae_layer *L, float **dx_dev) {
+  if (!L || !dx_dev) { set_error("NULL argument"); return LCAE_ERR_ARG; }
+  *dx_dev = L->dx_nhwc;
+  return LCAE_OK;
+}
+
+lcae_status lcae_counters(lcae_layer *L, int64_t *steps, int64_t *reinit_rows) {
+  if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
+  int r = 0;
+  LCAE_CK(cudaMemcpyAsync(&r, L->reinit_dev, sizeof(int), cudaMemcpyDeviceToHost, L->st));
+  LCAE_CK(cudaStreamSynchronize(L->st));
+  if (steps) *steps = L->steps;
+  if (reinit_rows) *reinit_rows = r;
+  return LCAE_OK;
+}
+
+int32_t lcae_last_launch_count(lcae_layer *L) { return L ? L->launches : 0; }
+
+}  // extern "C"

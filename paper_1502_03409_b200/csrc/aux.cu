@@ -1,0 +1,200 @@
+// aux.cu — layout conversion, loss reduction, parameter init/readback and the halo overlap-add kernel.
+// All HBM-bound; grid-stride loops sized to a multiple of the SM count.
+#include "common.cuh"
+
+namespace lcae {
+namespace {
+
+// NHWC [m][P] -> HWCN [P][m] (P = H*W*C): 32x32 tiled transpose through shared memory.
+template <typename T>
+__global__ void nhwc_to_hwcn(const float *__restrict__ x, T *__restrict__ xt, int m, int64_t P) {
+  __shared__ float tile[32][33];
+  const int64_t p0 = (int64_t)blockIdx.x * 32;
+  const int i0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    int i = i0 + r;
+    int64_t p = p0 + threadIdx.x;
+    tile[r][threadIdx.x] = (i < m && p < P) ? x[(int64_t)i * P + p] : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    int64_t p = p0 + r;
+    int i = i0 + threadIdx.x;
+    if (i < m && p < P) {
+      float v = tile[threadIdx.x][r];
+      if constexpr (sizeof(T) == 2) xt[p * m + i] = __float2bfloat16_rn(v);
+      else xt[p * m + i] = v;
+    }
+  }
+}
+
+__global__ void hwcn_to_nhwc(const float *__restrict__ xt, float *__restrict__ x, int m, int64_t P) {
+  __shared__ float tile[32][33];
+  const int64_t p0 = (int64_t)blockIdx.x * 32;
+  const int i0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    int64_t p = p0 + r;
+    int i = i0 + threadIdx.x;
+    tile[r][threadIdx.x] = (i < m && p < P) ? xt[p * m + i] : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    int i = i0 + r;
+    int64_t p = p0 + threadIdx.x;
+    if (i < m && p < P) x[(int64_t)i * P + p] = tile[threadIdx.x][r];
+  }
+}
+
+// Fixed-order fp64 reduction of the per-field loss partials [F][2] -> loss[2].
+__global__ void __launch_bounds__(1024) loss_reduce(const double *part, int F, double *out) {
+  __shared__ double sh[32];
+  double a = 0.0, b = 0.0;
+  for (int f = threadIdx.x; f < F; f += blockDim.x) { a += part[2 * f]; b += part[2 * f + 1]; }
+  double ta = block_sum_f64(a, sh);
+  __syncthreads();
+  double tb = block_sum_f64(b, sh);
+  if (threadIdx.x == 0) { out[0] = ta; out[1] = tb; }
+}
+
+// Default init: counter-based uniform rows (unit length), alpha = alpha_init, b = 0, sigma = 1.
+__global__ void __launch_bounds__(256) init_rows(Geo g, float *W, float *sigma, uint64_t seed) {
+  __shared__ double sh[32];
+  __shared__ float s_sc;
+  const int f = blockIdx.x, j = blockIdx.y;
+  float *w = W + ((int64_t)f * g.k + j) * g.n;
+  uint64_t key = splitmix64(seed ^ 0x5EEDull ^ ((uint64_t)f << 20) ^ (uint64_t)j);
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < g.n; t += blockDim.x) {
+    float u = (float)((double)(splitmix64(key + t) >> 40) / 16777216.0 - 0.5);
+    w[t] = u;
+    acc += (double)u * u;
+  }
+  double tot = block_sum_f64(acc, sh);
+  if (threadIdx.x == 0) s_sc = (float)(1.0 / sqrt(tot));
+  __syncthreads();
+  for (int t = threadIdx.x; t < g.n; t += blockDim.x) w[t] *= s_sc;
+  if (threadIdx.x == 0) sigma[(int64_t)f * g.k + j] = 1.f;
+}
+
+__global__ void fill_f32(float *p, int64_t n, float v) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) p[t] = v;
+}
+
+// W_out[f][j][t] = sigma[f][j] * W~[f][j][t]
+__global__ void get_w(Geo g, const float *W, const float *sigma, float *out) {
+  const int64_t tot = (int64_t)g.F * g.k * g.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = W[t] * sigma[t / g.n];
+}
+
+// bf16 shadow [F][k][n_al] of W~ (pad columns zero).
+__global__ void shadow_w(Geo g, int n_al, const float *W, __nv_bfloat16 *Wb) {
+  const int64_t tot = (int64_t)g.F * g.k * n_al;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t row = t / n_al;
+    int col = (int)(t - row * n_al);
+    Wb[t] = __float2bfloat16_rn(col < g.n ? W[row * g.n + col] : 0.f);
+  }
+}
+
+__global__ void region_add(float *dst, int dst_h, int dst_w, const float *src, int m, int rows, int cols, int C,
+                           int y0, int x0) {
+  const int64_t per = (int64_t)rows * cols * C, tot = per * m;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / per, r = t - i * per;
+    int c = (int)(r % C);
+    int64_t yx = r / C;
+    int x = (int)(yx % cols), y = (int)(yx / cols);
+    dst[((i * dst_h + y0 + y) * dst_w + x0 + x) * C + c] += src[t];
+  }
+}
+
+__global__ void check_finite(const float *x, int64_t n, int *flag) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(x[t])) { *flag = 1; return; }
+}
+
+}  // namespace
+
+lcae_status launch_nhwc_to_hwcn_f32(lcae_layer *L, const float *x, float *xt) {
+  const Geo &g = L->geo;
+  int64_t P = (int64_t)g.H * g.W * g.C;
+  dim3 grid((unsigned)cdiv((int)P, 32), cdiv(g.m, 32));
+  nhwc_to_hwcn<float><<<grid, dim3(32, 8), 0, L->st>>>(x, xt, g.m, P);
+  LCAE_CK_LAUNCH(L);
+  return LCAE_OK;
+}
+
+lcae_status launch_nhwc_to_hwcn_bf16(lcae_layer *L, const float *x, __nv_bfloat16 *xt) {
+  const Geo &g = L->geo;
+  int64_t P = (int64_t)g.H * g.W * g.C;
+  dim3 grid((unsigned)cdiv((int)P, 32), cdiv(g.m, 32));
+  nhwc_to_hwcn<__nv_bfloat16><<<grid, dim3(32, 8), 0, L->st>>>(x, xt, g.m, P);
+  LCAE_CK_LAUNCH(L);
+  return LCAE_OK;
+}
+
+lcae_status launch_hwcn_to_nhwc_f32(lcae_layer *L, const float *xt, float *x) {
+  const Geo &g = L->geo;
+  int64_t P = (int64_t)g.H * g.W * g.C;
+  dim3 grid((unsigned)cdiv((int)P, 32), cdiv(g.m, 32));
+  hwcn_to_nhwc<<<grid, dim3(32, 8), 0, L->st>>>(xt, x, g.m, P);
+  LCAE_CK_LAUNCH(L);
+  return LCAE_OK;
+}
+
+lcae_status launch_loss_reduce(lcae_layer *L) {
+  loss_reduce<<<1, 1024, 0, L->st>>>(L->loss_part, L->geo.F, L->loss_dev);
+  LCAE_CK_LAUNCH(L);
+  return LCAE_OK;
+}
+
+lcae_status launch_init_params(lcae_layer *L) {
+  const Geo &g = L->geo;
+  init_rows<<<dim3(g.F, g.k), 256, 0, L->st>>>(g, L->W, L->sigma, L->cfg.seed);
+  LCAE_CK_LAUNCH(L);
+  fill_f32<<<L->sm_count, 256, 0, L->st>>>(L->alpha, g.F, L->cfg.alpha_init);
+  LCAE_CK_LAUNCH(L);
+  LCAE_CK(cudaMemsetAsync(L->b, 0, (size_t)g.F * g.n * 4, L->st));
+  return LCAE_OK;
+}
+
+lcae_status launch_fill(lcae_layer *L, float *p, int64_t n, float v) {
+  fill_f32<<<L->sm_count, 256, 0, L->st>>>(p, n, v);
+  LCAE_CK_LAUNCH(L);
+  return LCAE_OK;
+}
+
+lcae_status launch_get_W(lcae_layer *L, float *Wout) {
+  get_w<<<L->sm_count * 8, 256, 0, L->st>>>(L->geo, L->W, L->sigma, Wout);
+  LCAE_CK_LAUNCH(L);
+  return LCAE_OK;
+}
+
+lcae_status launch_refresh_shadow(lcae_layer *L) {
+  if (!L->Wb) return LCAE_OK;
+  shadow_w<<<L->sm_count * 8, 256, 0, L->st>>>(L->geo, L->n_al, L->W, L->Wb);
+  LCAE_CK_LAUNCH(L);
+  return LCAE_OK;
+}
+
+lcae_status launch_check_finite(lcae_layer *L, const float *x, int64_t count, int *flag) {
+  check_finite<<<L->sm_count * 4, 256, 0, L->st>>>(x, count, flag);
+  LCAE_CK_LAUNCH(L);
+  return LCAE_OK;
+}
+
+}  // namespace lcae
+
+extern "C" lcae_status lcae_region_add(void *stream, float *dst, int32_t dst_h, int32_t dst_w, const float *src,
+                                       int32_t m, int32_t rows, int32_t cols, int32_t C, int32_t y0, int32_t x0) {
+  if (!dst || !src) { lcae::set_error("lcae_region_add: NULL pointer"); return LCAE_ERR_ARG; }
+  if (m <= 0 || rows <= 0 || cols <= 0 || C <= 0 || y0 < 0 || x0 < 0 || y0 + rows > dst_h || x0 + cols > dst_w) {
+    lcae::set_error("lcae_region_add: region outside destination");
+    return LCAE_ERR_ARG;
+  }
+  lcae::region_add<<<148 * 4, 256, 0, (cudaStream_t)stream>>>(dst, dst_h, dst_w, src, m, rows, cols, C, y0, x0);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { lcae::set_error(cudaGetErrorString(e)); return LCAE_ERR_CUDA; }
+  return LCAE_OK;
+}

@@ -1,0 +1,68 @@
+"""GPU (through the C ABI) vs fp64 oracle, element by element, on identical seeded inputs.
+
+Tolerances (BASELINE.json north_star; R10, normwise ||gpu - oracle||_inf / ||oracle||_inf):
+fp32 path <= 1e-5, bf16 tensor-core path <= 2e-2, per tensor: loss, pooled code, dW, dalpha, db, dX and the
+parameter update (W' - W, alpha' - alpha, b' - b).  Row norms after the update: |‖W_j‖ - 1| <= 1e-6 (fp32 master).
+"""
+import numpy as np
+import pytest
+
+from paper_1502_03409_b200.inputs import CONFIGS, LayerShape, make_images, make_params
+from tests.gpu_harness import gpu_step, oracle_step
+from tests.helpers import normwise
+
+pytestmark = pytest.mark.gpu
+
+TOL = {0: 1e-5, 1: 2e-2}
+
+SHAPES = {
+    "c1": CONFIGS["c1"],
+    "c2": CONFIGS["c2"],
+    # ragged: n = 5*7*2 = 70 (not a multiple of 16/64), k = 24, g = 4, odd batch, non-square image
+    "ragged": LayerShape("ragged", 21, 25, 2, 5, 7, 2, 24, 4, 37),
+    "worked": LayerShape("worked", 2, 1, 1, 2, 1, 1, 2, 1, 1, eps=0.0),
+}
+
+
+def _compare(shape, precision, out, o, W, a, b):
+    tol = TOL[precision]
+    errs = {}
+    errs["J"] = abs(out["J"] - o["J"]) / abs(o["J"])
+    errs["J_rec"] = abs(out["J_rec"] - o["J_rec"]) / abs(o["J_rec"]) if o["J_rec"] else abs(out["J_rec"])
+    errs["J_sparse"] = abs(out["J_sparse"] - o["J_sparse"]) / abs(o["J_sparse"])
+    if "p" in out:
+        errs["p"] = normwise(out["p"], o["p"])
+        errs["J_fwd"] = abs(out["J_fwd"] - o["J"]) / abs(o["J"])
+    for key in ("dW", "dalpha", "db", "dX"):
+        if key in out:
+            errs[key] = normwise(out[key], o[key])
+    errs["dW_update"] = normwise(out["W_new"].astype(np.float64) - W, o["W_new"] - W)
+    errs["alpha_update"] = normwise(out["alpha_new"].astype(np.float64) - a, o["alpha_new"] - a)
+    errs["b_update"] = normwise(out["b_new"].astype(np.float64) - b, o["b_new"] - b)
+    bad = {k: v for k, v in errs.items() if not (v <= tol)}
+    assert not bad, (shape.name, precision, bad, errs)
+    norms = np.linalg.norm(out["W_new"].astype(np.float64), axis=-1)
+    assert np.abs(norms - 1).max() <= 1e-6
+    return errs
+
+
+@pytest.mark.parametrize("name", ["worked", "c1", "ragged", "c2"])
+def test_fp32_parity(name):
+    shape = SHAPES[name]
+    if name == "worked":   # SPEC.md:97 instance through the whole GPU pipeline
+        W = np.eye(2, dtype=np.float32)[None]
+        a = np.array([2.0], np.float32)
+        b = np.zeros((1, 2), np.float32)
+        X = np.array([1.0, -1.0], np.float32).reshape(1, 2, 1, 1)
+    else:
+        W, a, b = make_params(shape, seed=0)
+        X = make_images(shape, seed=1)
+        b = (0.05 * np.random.default_rng(3).standard_normal(b.shape)).astype(np.float32)
+    out = gpu_step(shape, 0, W, a, b, X)
+    o = oracle_step(shape, W, a, b, X)
+    _compare(shape, 0, out, o, W.astype(np.float64), a.astype(np.float64), b.astype(np.float64))
+    if name == "worked":
+        assert out["J"] == pytest.approx(2.4, rel=1e-6)
+        np.testing.assert_allclose(out["dW"][0], [[8.2, -8.2], [-8.2, 8.2]], rtol=1e-6)
+    assert out["steps"] == 1 and out["reinit"] == 0
+    assert out["launches"] > 0
