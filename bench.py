@@ -1,0 +1,276 @@
+"""Benchmark of one training step of the locally-connected RICA autoencoder layer (BASELINE.json metric:
+images/sec per LC-autoencoder training step, TFLOP/s vs B200 peak).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c1] [--impl ours|reference]
+
+A step = one pass of the whole hot path (input staging, encode, L2 pooling +
+sparsity, decode + residual, loss reduction, backprop into the code, weight gradient, input gradient with
+overlap-add, fused projected-SGD update) over one batch of synthetic whitened images, through the C ABI.
+N = 1: the whole layer on one GPU.  N > 1 (torchrun): the field grid is tiled over ranks (parallel.py);
+every rank runs its tile, halos travel over NCCL; value = images/s of the whole job (model parallel: every
+rank sees every image), time = max over ranks.
+
+--impl reference: the fp64 CPU oracle (oracle/), as it stands, timed on this host on a bounded sample of
+the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from paper_1502_03409_b200.inputs import CONFIGS, make_images, make_params, stratified_fields  # noqa: E402
+
+METRIC = "images/sec per LC-autoencoder training step"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d["bf16_tflops_sustained"], src="measured")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+def model_flops(shape):
+    """12 k n m F: encode, decode, backprop-to-code, two weight-gradient products, input gradient."""
+    return 12.0 * shape.filters * shape.n * shape.batch * shape.fields
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+
+    def __init__(self, index=0, period=0.05):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period, self.index = period, index
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception as e:  # pragma: no cover
+            self.nv = None
+            self.err = str(e)
+        return self
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, nm in names.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_oracle_rate(shape, budget_s=12.0, seed=0):
+    """Time the fp64 oracle (as it stands) on a bounded field sample; return images/s extrapolated to the
+    whole layer (every field costs the same work) plus a description."""
+    from oracle import lcae_oracle as O
+    geo = dict(img_h=shape.img_h, img_w=shape.img_w, img_c=shape.img_c, rf_h=shape.rf_h, rf_w=shape.rf_w,
+               stride=shape.stride, pool_group=shape.pool_group, lam=shape.lam, eps=shape.eps)
+    X = make_images(shape, seed=1).astype(np.float64)
+    done, t_used = 0, 0.0
+    order = stratified_fields(shape, shape.fields, seed=seed)
+    while t_used < budget_s and done < shape.fields:
+        nb = min(max(1, done or 4), shape.fields - done)
+        fl = order[done:done + nb]
+        W, a, b = make_params(shape, seed=0, fields=fl)
+        t0 = time.perf_counter()
+        O.step(W.astype(np.float64), a.astype(np.float64), b.astype(np.float64), X, geo, lr=shape.lr, fields=fl)
+        t_used += time.perf_counter() - t0
+        done += nb
+    t_step = t_used * shape.fields / done
+    try:
+        threads = len(os.sched_getaffinity(0))
+    except Exception:
+        threads = os.cpu_count()
+    return shape.batch / t_step, done, t_used, threads
+
+
+def run_reference(args, shape):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = []
+    for _ in range(args.warmup):
+        cpu_oracle_rate(shape, budget_s=args.ref_budget / 4)
+    for _ in range(args.steps):
+        v, done, t_used, threads = cpu_oracle_rate(shape, budget_s=args.ref_budget)
+        steps.append((v, done, t_used))
+    v = statistics.median(s[0] for s in steps)
+    sample = (f"{steps[0][1]} of {shape.fields} fields per step (stratified), extrapolated linearly; "
+              f"fp64 numpy oracle, {steps[0][2]:.1f} s per sample")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "images/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * shape.batch / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": shape.name, "image": [shape.img_h, shape.img_w, shape.img_c],
+                       "rf": shape.rf_h, "stride": shape.stride, "filters": shape.filters,
+                       "pool_group": shape.pool_group, "batch": shape.batch, "fields": shape.fields},
+            "cpu_baseline": {"value": v, "unit": "images/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, shape):
+    import torch
+    from paper_1502_03409_b200 import lcae
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_1502_03409_b200 import parallel
+        tile = parallel.plan(shape, world)[rank]
+        runner = parallel.TileRunner(shape, tile, world, rank)
+    stream = torch.cuda.Stream()
+    pk = peaks()
+    with torch.cuda.stream(stream):
+        if world == 1:
+            cfg = lcae.make_config(shape, precision=lcae.BF16, stream=stream.cuda_stream)
+            L = lcae.Layer(cfg)
+            W, a, b = make_params(shape, seed=0)
+            L.set_params(W, a, b)
+            del W
+            pool = [torch.from_numpy(make_images(shape, seed=1, index=i)).cuda() for i in range(4)]
+            step = lambda i: L.step(pool[i % len(pool)], None, want_loss=False)  # noqa: E731
+        else:
+            L = runner.layer
+            step = runner.bench_step_fn(stream)
+        torch.cuda.synchronize()
+        for i in range(args.warmup):
+            step(i)
+        torch.cuda.synchronize()
+        launches_per_step = L.last_launch_count() + (runner.extra_launches if world > 1 else 0)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        L.profile(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            for i in range(args.steps):
+                step(i)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        L.profile(False)
+        ms = e0.elapsed_time(e1)
+        kern_ms, kern_n = L.profile_read()
+        if dist:
+            t = torch.tensor([ms, kern_ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms, kern_ms = t.tolist()
+        ms_step = ms / args.steps
+        # ---- end to end through the C ABI with host buffers (pinned), loss read back every step
+        e2e = None
+        if world == 1:
+            hosts = [p.cpu().pin_memory() for p in pool[:2]]
+            h2d = hosts[0].numel() * 4
+            for i in range(2):
+                L.step(hosts[i % 2], None, want_loss=True)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            n_e2e = max(3, min(args.steps, 10))
+            for i in range(n_e2e):
+                L.step(hosts[i % 2], None, want_loss=True)
+            dt = (time.perf_counter() - t0) / n_e2e
+            e2e = {"value": shape.batch / dt, "unit": "images/s", "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": 8, "ms_per_step": dt * 1e3}
+    if rank != 0:
+        return
+    flops = model_flops(shape)
+    value = shape.batch / (ms_step * 1e-3)
+    kern_avg = kern_ms / max(1, kern_n)
+    per_kernel_flops = flops / world
+    achieved = per_kernel_flops / (kern_avg * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": shape.name, "image": [shape.img_h, shape.img_w, shape.img_c], "rf": shape.rf_h,
+                   "stride": shape.stride, "filters": shape.filters, "pool_group": shape.pool_group,
+                   "batch": shape.batch, "fields": shape.fields, "params": shape.fields * shape.filters * shape.n,
+                   "parallelism": f"mp{world}" if world > 1 else "single",
+                   "l2": "working set > L2 (fp32 W master 4 B/param streamed every step)"},
+        "tflops": flops / (ms_step * 1e-3) / 1e12,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
+                     "frac": achieved / pk["bf16_sus"], "traffic": None,
+                     "kernel": "lcae::tc::step_kernel", "kernel_ms": kern_avg,
+                     "peak_source": f"{pk['src']} bf16_tflops_sustained (kernel timed inside a long step)"},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        v, done, t_used, threads = cpu_oracle_rate(shape, budget_s=args.ref_budget)
+        line["cpu_baseline"] = {"value": v, "unit": "images/s", "cores": threads, "kind": "oracle",
+                                "sample": f"{done} of {shape.fields} fields (stratified), {t_used:.1f} s, "
+                                          f"extrapolated linearly to the full layer"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of oracle work per sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    shape = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, shape)
+    else:
+        run_ours(args, shape)
+
+
+if __name__ == "__main__":
+    main()

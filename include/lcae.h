@@ -138,6 +138,13 @@ lcae_status lcae_region_add(void *stream, float *dst, int32_t dst_h, int32_t dst
 /* Kernel launches issued by the last lcae_step / lcae_forward on this handle (bench accounting). */
 int32_t lcae_last_launch_count(lcae_layer *L);
 
+/* Kernel timing for roofline accounting: enable = 1 starts recording CUDA events (on the layer's stream)
+ * around the dominant fused step kernel of every subsequent lcae_step (up to 4096 steps); enable = 0 stops.
+ * lcae_profile_read synchronises and returns the summed duration (ms) and the number of recorded launches,
+ * then clears the record. Events add no synchronisation inside the step. */
+lcae_status lcae_profile(lcae_layer *L, int32_t enable);
+lcae_status lcae_profile_read(lcae_layer *L, double *main_kernel_ms, int32_t *launches);
+
 /* Thread-local description of the last error (never NULL). */
 const char *lcae_last_error(void);
 

@@ -132,6 +132,10 @@ lcae_status lcae_destroy(lcae_layer *L) {
                   (void *)L->rowsq})
     if (p) cudaFree(p);
   if (L->loss_host) cudaFreeHost(L->loss_host);
+  if (L->prof_ev) {
+    for (int i = 0; i < 2 * 4096; ++i) cudaEventDestroy(L->prof_ev[i]);
+    delete[] L->prof_ev;
+  }
   delete L;
   return LCAE_OK;
 }
@@ -176,8 +180,10 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
     CKF(cudaMemsetAsync(L->va, 0, F * 4, L->st));
     CKF(cudaMemsetAsync(L->vb, 0, F * n * 4, L->st));
   }
+  L->mp = cfg->precision == LCAE_FP32 ? g.m : (g.m + 7) / 8 * 8;
+  const size_t mp = L->mp;
   CKF(cudaMalloc(&L->x_stage, m * img * 4));
-  CKF(cudaMalloc(&L->dxt, m * img * 4));
+  CKF(cudaMalloc(&L->dxt, mp * img * 4));
   CKF(cudaMalloc(&L->dx_nhwc, m * img * 4));
   CKF(cudaMalloc(&L->pooled, m * F * (k / g.g) * 4));
   CKF(cudaMalloc(&L->loss_part, F * 2 * sizeof(double)));
@@ -196,8 +202,8 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
     FAIL(f32_alloc(L));
   } else {
     L->n_al = (int)((n + 7) / 8 * 8);
-    CKF(cudaMalloc(&L->Wb, F * k * (size_t)L->n_al * 2));
-    CKF(cudaMalloc(&L->xt16, m * img * 2));
+    CKF(cudaMalloc(&L->xt16, mp * img * 2));
+    CKF(cudaMemset(L->xt16, 0, mp * img * 2));   // padded batch columns stay zero
     CKF(cudaMalloc(&L->rowsq, F * k * 4));
     FAIL(tc_alloc(L));
   }
@@ -317,5 +323,30 @@ lcae_status lcae_counters(lcae_layer *L, int64_t *steps, int64_t *reinit_rows) {
 }
 
 int32_t lcae_last_launch_count(lcae_layer *L) { return L ? L->launches : 0; }
+
+lcae_status lcae_profile(lcae_layer *L, int32_t enable) {
+  if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
+  if (enable && !L->prof_ev) {
+    L->prof_ev = new cudaEvent_t[2 * 4096];
+    for (int i = 0; i < 2 * 4096; ++i) LCAE_CK(cudaEventCreate(&L->prof_ev[i]));
+  }
+  L->prof_on = enable ? 1 : 0;
+  return LCAE_OK;
+}
+
+lcae_status lcae_profile_read(lcae_layer *L, double *main_kernel_ms, int32_t *launches) {
+  if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
+  double tot = 0.0;
+  if (L->prof_n) LCAE_CK(cudaEventSynchronize(L->prof_ev[2 * L->prof_n - 1]));
+  for (int i = 0; i < L->prof_n; ++i) {
+    float ms = 0.f;
+    LCAE_CK(cudaEventElapsedTime(&ms, L->prof_ev[2 * i], L->prof_ev[2 * i + 1]));
+    tot += ms;
+  }
+  if (main_kernel_ms) *main_kernel_ms = tot;
+  if (launches) *launches = L->prof_n;
+  L->prof_n = 0;
+  return LCAE_OK;
+}
 
 }  // extern "C"

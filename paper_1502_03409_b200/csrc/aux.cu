@@ -7,7 +7,7 @@ namespace {
 
 // NHWC [m][P] -> HWCN [P][m] (P = H*W*C): 32x32 tiled transpose through shared memory.
 template <typename T>
-__global__ void nhwc_to_hwcn(const float *__restrict__ x, T *__restrict__ xt, int m, int64_t P) {
+__global__ void nhwc_to_hwcn(const float *__restrict__ x, T *__restrict__ xt, int m, int mp, int64_t P) {
   __shared__ float tile[32][33];
   const int64_t p0 = (int64_t)blockIdx.x * 32;
   const int i0 = blockIdx.y * 32;
@@ -22,20 +22,20 @@ __global__ void nhwc_to_hwcn(const float *__restrict__ x, T *__restrict__ xt, in
     int i = i0 + threadIdx.x;
     if (i < m && p < P) {
       float v = tile[threadIdx.x][r];
-      if constexpr (sizeof(T) == 2) xt[p * m + i] = __float2bfloat16_rn(v);
-      else xt[p * m + i] = v;
+      if constexpr (sizeof(T) == 2) xt[p * mp + i] = __float2bfloat16_rn(v);
+      else xt[p * mp + i] = v;
     }
   }
 }
 
-__global__ void hwcn_to_nhwc(const float *__restrict__ xt, float *__restrict__ x, int m, int64_t P) {
+__global__ void hwcn_to_nhwc(const float *__restrict__ xt, float *__restrict__ x, int m, int mp, int64_t P) {
   __shared__ float tile[32][33];
   const int64_t p0 = (int64_t)blockIdx.x * 32;
   const int i0 = blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += 8) {
     int64_t p = p0 + r;
     int i = i0 + threadIdx.x;
-    tile[r][threadIdx.x] = (i < m && p < P) ? xt[p * m + i] : 0.f;
+    tile[r][threadIdx.x] = (i < m && p < P) ? xt[p * mp + i] : 0.f;
   }
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += 8) {
@@ -46,7 +46,7 @@ __global__ void hwcn_to_nhwc(const float *__restrict__ xt, float *__restrict__ x
 }
 
 // Fixed-order fp64 reduction of the per-field loss partials [F][2] -> loss[2].
-__global__ void __launch_bounds__(1024) loss_reduce(const double *part, int F, double *out) {
+__global__ void __launch_bounds__(1024) loss_reduce(const double *part, int F, double *out) {  // F = #partial pairs
   __shared__ double sh[32];
   double a = 0.0, b = 0.0;
   for (int f = threadIdx.x; f < F; f += blockDim.x) { a += part[2 * f]; b += part[2 * f + 1]; }
@@ -87,13 +87,14 @@ __global__ void get_w(Geo g, const float *W, const float *sigma, float *out) {
     out[t] = W[t] * sigma[t / g.n];
 }
 
-// bf16 shadow [F][k][n_al] of W~ (pad columns zero).
-__global__ void shadow_w(Geo g, int n_al, const float *W, __nv_bfloat16 *Wb) {
-  const int64_t tot = (int64_t)g.F * g.k * n_al;
+// bf16 shadow [F][kp][n_al] of W~ (pad rows and columns zero).
+__global__ void shadow_w(Geo g, int kp, int n_al, const float *W, __nv_bfloat16 *Wb) {
+  const int64_t tot = (int64_t)g.F * kp * n_al;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t row = t / n_al;
     int col = (int)(t - row * n_al);
-    Wb[t] = __float2bfloat16_rn(col < g.n ? W[row * g.n + col] : 0.f);
+    int f = (int)(row / kp), r = (int)(row - (int64_t)f * kp);
+    Wb[t] = __float2bfloat16_rn(col < g.n && r < g.k ? W[((int64_t)f * g.k + r) * g.n + col] : 0.f);
   }
 }
 
@@ -120,7 +121,7 @@ lcae_status launch_nhwc_to_hwcn_f32(lcae_layer *L, const float *x, float *xt) {
   const Geo &g = L->geo;
   int64_t P = (int64_t)g.H * g.W * g.C;
   dim3 grid((unsigned)cdiv((int)P, 32), cdiv(g.m, 32));
-  nhwc_to_hwcn<float><<<grid, dim3(32, 8), 0, L->st>>>(x, xt, g.m, P);
+  nhwc_to_hwcn<float><<<grid, dim3(32, 8), 0, L->st>>>(x, xt, g.m, L->mp, P);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }
@@ -129,7 +130,7 @@ lcae_status launch_nhwc_to_hwcn_bf16(lcae_layer *L, const float *x, __nv_bfloat1
   const Geo &g = L->geo;
   int64_t P = (int64_t)g.H * g.W * g.C;
   dim3 grid((unsigned)cdiv((int)P, 32), cdiv(g.m, 32));
-  nhwc_to_hwcn<__nv_bfloat16><<<grid, dim3(32, 8), 0, L->st>>>(x, xt, g.m, P);
+  nhwc_to_hwcn<__nv_bfloat16><<<grid, dim3(32, 8), 0, L->st>>>(x, xt, g.m, L->mp, P);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }
@@ -138,13 +139,15 @@ lcae_status launch_hwcn_to_nhwc_f32(lcae_layer *L, const float *xt, float *x) {
   const Geo &g = L->geo;
   int64_t P = (int64_t)g.H * g.W * g.C;
   dim3 grid((unsigned)cdiv((int)P, 32), cdiv(g.m, 32));
-  hwcn_to_nhwc<<<grid, dim3(32, 8), 0, L->st>>>(xt, x, g.m, P);
+  hwcn_to_nhwc<<<grid, dim3(32, 8), 0, L->st>>>(xt, x, g.m, L->mp, P);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }
 
 lcae_status launch_loss_reduce(lcae_layer *L) {
-  loss_reduce<<<1, 1024, 0, L->st>>>(L->loss_part, L->geo.F, L->loss_dev);
+  const bool tcp = L->cfg.precision == LCAE_BF16;
+  loss_reduce<<<1, 1024, 0, L->st>>>(tcp ? tc_loss_part(L) : L->loss_part, tcp ? tc_loss_count(L) : L->geo.F,
+                                     L->loss_dev);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }
@@ -173,7 +176,7 @@ lcae_status launch_get_W(lcae_layer *L, float *Wout) {
 
 lcae_status launch_refresh_shadow(lcae_layer *L) {
   if (!L->Wb) return LCAE_OK;
-  shadow_w<<<L->sm_count * 8, 256, 0, L->st>>>(L->geo, L->n_al, L->W, L->Wb);
+  shadow_w<<<L->sm_count * 8, 256, 0, L->st>>>(L->geo, 128, L->n_al, L->W, L->Wb);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }

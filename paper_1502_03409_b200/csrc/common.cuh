@@ -64,6 +64,7 @@ struct lcae_layer {
   float *vW = nullptr, *va = nullptr, *vb = nullptr;   // momentum velocity (momentum > 0)
   __nv_bfloat16 *Wb = nullptr;                         // bf16 shadow [F][k][n_al] (bf16 mode)
   int n_al = 0;                                        // n rounded up to 8 (16-byte rows)
+  int mp = 0;                                          // batch stride of the internal HWCN buffers
   // inputs / outputs
   float *x_stage = nullptr;      // NHWC f32 staging for host inputs
   float *xt32 = nullptr;         // HWCN f32 (fp32 mode)
@@ -81,6 +82,9 @@ struct lcae_layer {
   int launches = 0;
   lcae::F32Scratch f32;
   lcae::TcScratch *tc = nullptr;
+  // profiling (lcae_profile): events around the dominant kernel
+  int prof_on = 0, prof_n = 0;
+  cudaEvent_t *prof_ev = nullptr;   // [2 * 4096]
 };
 
 namespace lcae {
@@ -125,6 +129,8 @@ lcae_status f32_step(lcae_layer *L, bool update, bool want_pooled);
 lcae_status tc_alloc(lcae_layer *L);
 void tc_free(lcae_layer *L);
 lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled);
+double *tc_loss_part(lcae_layer *L);
+int tc_loss_count(lcae_layer *L);
 
 // aux kernels (aux.cu)
 lcae_status launch_nhwc_to_hwcn_f32(lcae_layer *L, const float *x, float *xt);

@@ -122,7 +122,8 @@ using namespace lcae;
 extern "C" lcae_status lcae_dev_umma_selftest(int a_mn, int b_mn, int N, int K, int variant, const void *A,
                                               const void *B, float *D) {
   if (N % 16 || N < 16 || N > 256 || K % 64 || K > 128) { set_error("selftest: bad shape"); return LCAE_ERR_ARG; }
-  int smem = 128 * K * 2 + K * N * 2 + 1024;
+  int Npad = (N + 63) / 64 * 64;
+  int smem = 128 * K * 2 + K * Npad * 2 + 1024;
   LCAE_CK(cudaFuncSetAttribute(umma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   umma_selftest_kernel<<<1, 128, smem>>>(a_mn, b_mn, N, K, variant, (const __nv_bfloat16 *)A,
                                          (const __nv_bfloat16 *)B, D);

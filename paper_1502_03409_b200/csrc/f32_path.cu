@@ -306,7 +306,7 @@ lcae_status f32_step(lcae_layer *L, bool update, bool want_pooled) {
   const int64_t km = (int64_t)k * m, nm = (int64_t)n * m, kn = (int64_t)k * n;
   lcae_status st;
 #define TRY(x) do { if ((st = (x)) != LCAE_OK) return st; } while (0)
-  LCAE_CK(cudaMemsetAsync(L->dxt, 0, (size_t)g.H * g.W * g.C * m * 4, L->st));
+  LCAE_CK(cudaMemsetAsync(L->dxt, 0, (size_t)g.H * g.W * g.C * L->mp * 4, L->st));
   for (int f0 = 0; f0 < g.F; f0 += s.Fc) {
     const int Fc = std::min(s.Fc, g.F - f0);
     Patch X{L->xt32, f0, g.gc, g.RW, m, g.SRC_R, g.SRC_C, g.SY};

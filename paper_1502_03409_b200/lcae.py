@@ -58,6 +58,8 @@ def _load():
         "lcae_region_add": (C.c_int, [P, P, C.c_int32, C.c_int32, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                       C.c_int32, C.c_int32]),
         "lcae_last_launch_count": (C.c_int32, [P]),
+        "lcae_profile": (C.c_int, [P, C.c_int32]),
+        "lcae_profile_read": (C.c_int, [P, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
         "lcae_last_error": (C.c_char_p, []),
         "lcae_version": (C.c_char_p, []),
         "lcae_dev_umma_selftest": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P]),
@@ -77,6 +79,7 @@ lib = _load()
 ABI_SYMBOLS = ("lcae_config_default", "lcae_geometry", "lcae_create", "lcae_destroy", "lcae_set_params",
                "lcae_get_params", "lcae_get_grads", "lcae_forward", "lcae_step", "lcae_last_loss",
                "lcae_dx_device", "lcae_counters", "lcae_region_add", "lcae_last_launch_count",
+               "lcae_profile", "lcae_profile_read",
                "lcae_last_error", "lcae_version")
 
 
@@ -183,6 +186,14 @@ class Layer:
 
     def last_launch_count(self) -> int:
         return int(lib.lcae_last_launch_count(self.h))
+
+    def profile(self, enable: bool):
+        check(lib.lcae_profile(self.h, int(bool(enable))))
+
+    def profile_read(self):
+        ms, n = C.c_double(), C.c_int32()
+        check(lib.lcae_profile_read(self.h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
 
 def region_add(dst, src, y0: int, x0: int, stream=None):

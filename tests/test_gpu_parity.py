@@ -66,3 +66,34 @@ def test_fp32_parity(name):
         np.testing.assert_allclose(out["dW"][0], [[8.2, -8.2], [-8.2, 8.2]], rtol=1e-6)
     assert out["steps"] == 1 and out["reinit"] == 0
     assert out["launches"] > 0
+
+
+SHAPES_BF16 = {
+    "worked": SHAPES["worked"],
+    "c1": CONFIGS["c1"],
+    "ragged": SHAPES["ragged"],
+    "c2": CONFIGS["c2"],
+    # two-CTA cluster (m > 128, ragged second slice), pooling g = 2, n = 8*8*3 = 192
+    "cluster2": LayerShape("cluster2", 20, 20, 3, 8, 8, 4, 32, 2, 200),
+    # paper layer-1-like field shape (k = 128, g = 1) on a small image, two CTAs
+    "c3tiny": LayerShape("c3tiny", 22, 22, 3, 18, 18, 2, 128, 1, 256),
+}
+
+
+@pytest.mark.parametrize("name", list(SHAPES_BF16))
+def test_bf16_parity(name):
+    shape = SHAPES_BF16[name]
+    if name == "worked":
+        W = np.eye(2, dtype=np.float32)[None]
+        a = np.array([2.0], np.float32)
+        b = np.zeros((1, 2), np.float32)
+        X = np.array([1.0, -1.0], np.float32).reshape(1, 2, 1, 1)
+    else:
+        W, a, b = make_params(shape, seed=0)
+        X = make_images(shape, seed=1)
+        b = (0.05 * np.random.default_rng(3).standard_normal(b.shape)).astype(np.float32)
+    out = gpu_step(shape, 1, W, a, b, X)
+    o = oracle_step(shape, W, a, b, X)
+    errs = _compare(shape, 1, out, o, W.astype(np.float64), a.astype(np.float64), b.astype(np.float64))
+    print(name, {k_: f"{v:.1e}" for k_, v in errs.items()})
+    assert out["steps"] == 1 and out["reinit"] == 0
