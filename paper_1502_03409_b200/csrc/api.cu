@@ -168,15 +168,19 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
   CKF(cudaGetDevice(&L->device));
   CKF(cudaDeviceGetAttribute(&L->sm_count, cudaDevAttrMultiProcessorCount, L->device));
   const size_t F = g.F, k = g.k, n = g.n, m = g.m, img = (size_t)g.H * g.W * g.C;
-  CKF(cudaMalloc(&L->W, F * k * n * 4));
+  L->n_al = (int)((n + 7) / 8 * 8);
+  L->wp = cfg->precision == LCAE_FP32 ? (int)n : L->n_al;   // fp32 master row pitch (16-byte rows, bf16)
+  const size_t wp = L->wp;
+  CKF(cudaMalloc(&L->W, F * k * wp * 4));
+  CKF(cudaMemsetAsync(L->W, 0, F * k * wp * 4, L->st));
   CKF(cudaMalloc(&L->sigma, F * k * 4));
   CKF(cudaMalloc(&L->alpha, F * 4));
   CKF(cudaMalloc(&L->b, F * n * 4));
   if (cfg->momentum > 0.f) {
-    CKF(cudaMalloc(&L->vW, F * k * n * 4));
+    CKF(cudaMalloc(&L->vW, F * k * wp * 4));
     CKF(cudaMalloc(&L->va, F * 4));
     CKF(cudaMalloc(&L->vb, F * n * 4));
-    CKF(cudaMemsetAsync(L->vW, 0, F * k * n * 4, L->st));
+    CKF(cudaMemsetAsync(L->vW, 0, F * k * wp * 4, L->st));
     CKF(cudaMemsetAsync(L->va, 0, F * 4, L->st));
     CKF(cudaMemsetAsync(L->vb, 0, F * n * 4, L->st));
   }
@@ -193,7 +197,8 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
   CKF(cudaMemsetAsync(L->reinit_dev, 0, sizeof(int), L->st));
   CKF(cudaMallocHost(&L->loss_host, 2 * sizeof(double)));
   if (cfg->keep_grads) {
-    CKF(cudaMalloc(&L->gW, F * k * n * 4));
+    CKF(cudaMalloc(&L->gW, F * k * wp * 4));
+    CKF(cudaMemsetAsync(L->gW, 0, F * k * wp * 4, L->st));
     CKF(cudaMalloc(&L->galpha, F * 4));
     CKF(cudaMalloc(&L->gb, F * n * 4));
   }
@@ -201,7 +206,6 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
     CKF(cudaMalloc(&L->xt32, m * img * 4));
     FAIL(f32_alloc(L));
   } else {
-    L->n_al = (int)((n + 7) / 8 * 8);
     CKF(cudaMalloc(&L->xt16, mp * img * 2));
     CKF(cudaMemset(L->xt16, 0, mp * img * 2));   // padded batch columns stay zero
     CKF(cudaMalloc(&L->rowsq, F * k * 4));
@@ -221,7 +225,8 @@ lcae_status lcae_set_params(lcae_layer *L, const float *W, const float *alpha, c
   const Geo &g = L->geo;
   lcae_status s;
   if (W) {
-    if ((s = copy_any(L, L->W, W, (size_t)g.F * g.k * g.n * 4))) return s;
+    LCAE_CK(cudaMemcpy2DAsync(L->W, (size_t)L->wp * 4, W, (size_t)g.n * 4, (size_t)g.n * 4, (size_t)g.F * g.k,
+                              cudaMemcpyDefault, L->st));
     // W is taken as given: sigma = 1 (W~ = W)
     if ((s = launch_fill(L, L->sigma, (int64_t)g.F * g.k, 1.f))) return s;
     if ((s = launch_refresh_shadow(L))) return s;
@@ -259,7 +264,9 @@ lcae_status lcae_get_grads(lcae_layer *L, float *dW, float *dalpha, float *db) {
   if (!L->cfg.keep_grads) return config_error("lcae_get_grads needs keep_grads = 1");
   const Geo &g = L->geo;
   lcae_status s;
-  if (dW && (s = copy_any(L, dW, L->gW, (size_t)g.F * g.k * g.n * 4))) return s;
+  if (dW)
+    LCAE_CK(cudaMemcpy2DAsync(dW, (size_t)g.n * 4, L->gW, (size_t)L->wp * 4, (size_t)g.n * 4, (size_t)g.F * g.k,
+                              cudaMemcpyDefault, L->st));
   if (dalpha && (s = copy_any(L, dalpha, L->galpha, (size_t)g.F * 4))) return s;
   if (db && (s = copy_any(L, db, L->gb, (size_t)g.F * g.n * 4))) return s;
   LCAE_CK(cudaStreamSynchronize(L->st));

@@ -57,11 +57,11 @@ __global__ void __launch_bounds__(1024) loss_reduce(const double *part, int F, d
 }
 
 // Default init: counter-based uniform rows (unit length), alpha = alpha_init, b = 0, sigma = 1.
-__global__ void __launch_bounds__(256) init_rows(Geo g, float *W, float *sigma, uint64_t seed) {
+__global__ void __launch_bounds__(256) init_rows(Geo g, int wp, float *W, float *sigma, uint64_t seed) {
   __shared__ double sh[32];
   __shared__ float s_sc;
   const int f = blockIdx.x, j = blockIdx.y;
-  float *w = W + ((int64_t)f * g.k + j) * g.n;
+  float *w = W + ((int64_t)f * g.k + j) * wp;
   uint64_t key = splitmix64(seed ^ 0x5EEDull ^ ((uint64_t)f << 20) ^ (uint64_t)j);
   double acc = 0.0;
   for (int t = threadIdx.x; t < g.n; t += blockDim.x) {
@@ -81,20 +81,22 @@ __global__ void fill_f32(float *p, int64_t n, float v) {
 }
 
 // W_out[f][j][t] = sigma[f][j] * W~[f][j][t]
-__global__ void get_w(Geo g, const float *W, const float *sigma, float *out) {
+__global__ void get_w(Geo g, int wp, const float *W, const float *sigma, float *out) {
   const int64_t tot = (int64_t)g.F * g.k * g.n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x)
-    out[t] = W[t] * sigma[t / g.n];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / g.n;
+    out[t] = W[row * wp + (t - row * g.n)] * sigma[row];
+  }
 }
 
 // bf16 shadow [F][kp][n_al] of W~ (pad rows and columns zero).
-__global__ void shadow_w(Geo g, int kp, int n_al, const float *W, __nv_bfloat16 *Wb) {
+__global__ void shadow_w(Geo g, int kp, int n_al, int wp, const float *W, __nv_bfloat16 *Wb) {
   const int64_t tot = (int64_t)g.F * kp * n_al;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t row = t / n_al;
     int col = (int)(t - row * n_al);
     int f = (int)(row / kp), r = (int)(row - (int64_t)f * kp);
-    Wb[t] = __float2bfloat16_rn(col < g.n && r < g.k ? W[((int64_t)f * g.k + r) * g.n + col] : 0.f);
+    Wb[t] = __float2bfloat16_rn(col < g.n && r < g.k ? W[((int64_t)f * g.k + r) * wp + col] : 0.f);
   }
 }
 
@@ -154,7 +156,7 @@ lcae_status launch_loss_reduce(lcae_layer *L) {
 
 lcae_status launch_init_params(lcae_layer *L) {
   const Geo &g = L->geo;
-  init_rows<<<dim3(g.F, g.k), 256, 0, L->st>>>(g, L->W, L->sigma, L->cfg.seed);
+  init_rows<<<dim3(g.F, g.k), 256, 0, L->st>>>(g, L->wp, L->W, L->sigma, L->cfg.seed);
   LCAE_CK_LAUNCH(L);
   fill_f32<<<L->sm_count, 256, 0, L->st>>>(L->alpha, g.F, L->cfg.alpha_init);
   LCAE_CK_LAUNCH(L);
@@ -169,14 +171,14 @@ lcae_status launch_fill(lcae_layer *L, float *p, int64_t n, float v) {
 }
 
 lcae_status launch_get_W(lcae_layer *L, float *Wout) {
-  get_w<<<L->sm_count * 8, 256, 0, L->st>>>(L->geo, L->W, L->sigma, Wout);
+  get_w<<<L->sm_count * 8, 256, 0, L->st>>>(L->geo, L->wp, L->W, L->sigma, Wout);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }
 
 lcae_status launch_refresh_shadow(lcae_layer *L) {
   if (!L->Wb) return LCAE_OK;
-  shadow_w<<<L->sm_count * 8, 256, 0, L->st>>>(L->geo, 128, L->n_al, L->W, L->Wb);
+  shadow_w<<<L->sm_count * 8, 256, 0, L->st>>>(L->geo, 128, L->n_al, L->wp, L->W, L->Wb);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }

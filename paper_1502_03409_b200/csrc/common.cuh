@@ -65,6 +65,7 @@ struct lcae_layer {
   __nv_bfloat16 *Wb = nullptr;                         // bf16 shadow [F][k][n_al] (bf16 mode)
   int n_al = 0;                                        // n rounded up to 8 (16-byte rows)
   int mp = 0;                                          // batch stride of the internal HWCN buffers
+  int wp = 0;                                          // row pitch (floats) of W~, vW, gW
   // inputs / outputs
   float *x_stage = nullptr;      // NHWC f32 staging for host inputs
   float *xt32 = nullptr;         // HWCN f32 (fp32 mode)

@@ -93,6 +93,29 @@ __global__ void tma_selftest_kernel(const __grid_constant__ CUtensorMap tmap, in
   for (int i = threadIdx.x; i < bytes; i += blockDim.x) dump[i] = smem[i];
 }
 
+// TMA box landing at an arbitrary 128-byte row offset inside a 1024-byte swizzle atom (the X gather of the
+// step kernel places runs of patch rows this way): dump the whole 16-row region.
+__global__ void tma_offset_selftest_kernel(const __grid_constant__ CUtensorMap tmap, int box_rows, int r0, int c0,
+                                           int dst_row, uint8_t *dump) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar;
+  for (int i = threadIdx.x; i < 64 * 128; i += blockDim.x) smem[i] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbar_init();
+  }
+  ptx::fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ptx::mbar_arrive_expect_tx(&bar, box_rows * 128);
+    ptx::tma_load_2d(smem + dst_row * 128, &tmap, &bar, c0, r0);
+  }
+  ptx::mbar_wait(&bar, 0);
+  for (int i = threadIdx.x; i < 64 * 128; i += blockDim.x) dump[i] = smem[i];
+}
+
 // Throughput probe: every thread issues `reps` fp32 reductions (mode 0: red.global.add.f32 coalesced,
 // mode 1: red.global.add.v4.f32, mode 2: plain ld+add+st) over a buffer of n floats.
 __global__ void red_probe_kernel(float *buf, int64_t n, int reps, int mode) {
@@ -156,5 +179,17 @@ extern "C" lcae_status lcae_dev_red_probe(float *buf, int64_t n, int reps, int m
   LCAE_CK(cudaEventElapsedTime(ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  return LCAE_OK;
+}
+
+extern "C" lcae_status lcae_dev_tma_offset_selftest(const void *src, int rows, int cols, int box_rows, int r0, int c0,
+                                                    int dst_row, uint8_t *dump) {
+  CUtensorMap m;
+  if (!make_tmap_2d_bf16(&m, src, rows, cols, cols, box_rows)) { set_error("tensor map encode failed"); return LCAE_ERR_CUDA; }
+  int smem = 64 * 128 + 1024;
+  LCAE_CK(cudaFuncSetAttribute(tma_offset_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  tma_offset_selftest_kernel<<<1, 128, smem>>>(m, box_rows, r0, c0, dst_row, dump);
+  LCAE_CK(cudaGetLastError());
+  LCAE_CK(cudaDeviceSynchronize());
   return LCAE_OK;
 }

@@ -1,0 +1,735 @@
+// tc_kernel.cuh — the fused bf16 tcgen05 training-step kernel of the locally-connected RICA layer (sm_100a).
+//
+// One persistent kernel does the whole per-field chain of PAPER.md:88: a cluster of
+// CB CTAs (CB = ceil(m/128); CTA c owns samples [128c, 128c+128)) walks the fields; for field f every CTA
+// streams bf16 W~_f tiles (TMA, 128B swizzle, 4-stage ring) and its X_f patch rows (cp.async gather from the
+// batch-innermost HWCN image) in three passes over n-tiles of 64:
+//
+//   pass 0  U^T   = X^T W~^T                   (M = samples, N = k, K = n)      TMEM [0,128)
+//           E0: u = sigma.U~, h = alpha u, s_G = sqrt(eps + sum_G h^2), J_s, p; H' = bf16(sigma.h) -> smem
+//   pass 1  R^T_j - X_j^T = H'^T W~_j + X_j^T (-I)   (M = samples, N = 64)       TMEM [128,384) (4 buffers)
+//           E1: e = (R - x) + b, J_r, delta = 2e -> smem (bf16), db partial (butterfly column sums)
+//           G^T  += delta_j^T W~_j^T  (lag 2)  (M = samples, N = k, K = 64)     TMEM [384,512)
+//           E1b: D = sigma.G~ + lambda h/s, dalpha, D' = bf16(sigma alpha D) -> smem
+//   pass 2  R^T_j - X_j^T (recompute delta), dX^T_j = D'^T W~_j; dx = dX - delta -> red.global.v4 into dX
+//           dW_j = H' delta_j^T + D' X_j^T     (M = k, N = 64, K = 2 x samples) TMEM 2 x [R|dX|dW]
+//           E2: sum the batch slices of dW_j over the cluster (DSMEM), projected-SGD of W~ (fp32 master +
+//               bf16 shadow, 16-byte vectors), row sums of squares for the new row scale sigma.
+//
+// The "- x" of the residual is accumulated by the tensor core (X_j^T times a constant -I tile; exact in
+// bf16/fp32), so the epilogue never touches x.
+// W = sigma (.) W~ with a per-row scale sigma ("lazy projection"): the unit-norm projection of
+// PAPER.md:89 is applied by the finalize kernel as sigma' = 1/||W~'_row||, so the update never re-reads W.
+//
+// Warp roles: 0 = W TMA producer, 1 = MMA issuer (one lane), 2-9 = epilogue (TMEM lane quarter = warp % 4,
+// column half = (warp - 2) / 4), 10 = X cp.async producer. X tiles of pass 0 borrow the D'/delta buffers (idle
+// during pass 0) as a 4-slot ring, those of pass 1 the D' buffer, those of pass 2 a dedicated 2-slot ring.
+#pragma once
+#include <algorithm>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace lcae {
+namespace tc {
+
+constexpr int KP = 128;        // filters padded to one TMEM lane block
+constexpr int NT = 64;         // n-tile
+constexpr int MC = 128;        // samples per CTA
+constexpr int NW = 4;          // W ring stages
+constexpr int NX = 2;          // pass-2 X ring stages
+constexpr int NP0 = 4;         // pass-0 X ring slots (D'[0..1], delta[0..1])
+constexpr int NRB = 4;         // pass-1 R buffers
+constexpr int GLAG = 2;        // G_j issued after R_{j+GLAG}
+constexpr int NEPI = 8;        // epilogue warps
+constexpr int XWARP = 2 + NEPI;
+constexpr int NTHREADS = 32 * (XWARP + 1);
+constexpr int MAX_NPAD = 1024;
+
+constexpr int NXMAP = 7;       // X tensor maps with box heights 1, 2, 4, ..., 64 rows
+constexpr int XPMAX = 64;      // max TMA pieces per 64-row X tile
+
+struct Params {
+  CUtensorMap tmW;   // W~ bf16 [F*KP][n_al], box (64, 128)
+  CUtensorMap tmX[NXMAP];   // X HWCN bf16 viewed as [H*W*C rows][mp], box (64 samples, 2^i rows)
+  const uint32_t *xpieces;  // [T][XPMAX]: off (16 b) | dst row (8 b) << 16 | log2 rows (8 b) << 24; 0xFFFFFFFF ends
+  Geo g;
+  int T, mp, CB, n_al, wp, mode, want_pooled, keep_grads;
+  float lam, eps, lr, mu;
+  const __nv_bfloat16 *xt;
+  float *dxt;
+  float *W;
+  const float *sigma, *alpha, *b;
+  __nv_bfloat16 *Wb;
+  float *vW, *pooled;
+  double *loss_part;   // [F][CB][2]
+  float *da_part;      // [F][CB]
+  float *db_part;      // [F][CB][n]
+  float *rowsq_part;   // [F][CB][KP]
+  float *gW;
+  unsigned long long *trace;   // nullable: per-role wait cycles summed over CTAs
+};
+
+struct __align__(1024) Smem {
+  uint8_t Wr[NW][16384];
+  uint8_t Xr[NX][16384];
+  uint8_t H[32768];
+  uint8_t D[32768];          // pass 0: X slots 0,1; pass 1: X ring
+  uint8_t Dl[2][16384];      // pass 0: X slots 2,3
+  uint8_t negI[8192];        // -I (64 x 64 bf16, SW128)
+  float recv[2][128][16];    // peer's dW partial for this CTA's owned 16-column chunks, [half][row][col]
+  uint16_t off[MAX_NPAD];    // pixel-feature offset of patch row n inside the field window (host-checked < 2^16)
+  float bs[MAX_NPAD];        // b_f of the current field (epilogue)
+  float sig[KP];
+  float dbw[2][NEPI][32];
+  double redd[NEPI][2];
+  float redf[NEPI];
+  uint64_t wfull[NW], wempty[NW], xfull[NX], xempty[NX], p0full[NP0], p0empty[NP0], p1full[2], p1empty[2];
+  uint64_t p0_ok, u_full, h_ready, g_full, d_ready, tmem_free;
+  uint64_t r_full[NRB], r_empty[NRB], dl_full[2], dl_empty[2];
+  uint64_t p2_rdx[2], p2_dw[2], p2_empty[2];
+  uint64_t recv_full, peer_free;
+  uint32_t tmem_base;
+  unsigned long long tr[32];   // optional wait-cycle trace (lcae_dev_trace)
+};
+
+__device__ __forceinline__ uint8_t *p0slot(Smem &S, int i) { return i < 2 ? S.D + i * 16384 : S.Dl[i - 2]; }
+
+// store 8 consecutive bf16 (cols c0..c0+7 of row `row`) into a [rows][64] SW128 block
+__device__ __forceinline__ void st8(uint8_t *blk, int row, int c0, const float *v) {
+  uint4 q;
+  q.x = ptx::pack_bf16x2(v[0], v[1]);
+  q.y = ptx::pack_bf16x2(v[2], v[3]);
+  q.z = ptx::pack_bf16x2(v[4], v[5]);
+  q.w = ptx::pack_bf16x2(v[6], v[7]);
+  *reinterpret_cast<uint4 *>(blk + ptx::sw128_off(row, c0)) = q;
+}
+
+__device__ __forceinline__ void red_v4(float *p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+// e = (R - x) + b over this warp's 32 columns of a tile for this thread's sample; rv <- delta = 2e (masked).
+__device__ __forceinline__ float residual32(float (&rv)[32], int c0, int n, const float *bf_, bool svalid) {
+  float jr = 0.f;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const int nn = c0 + c;
+    const float bv = nn < n ? bf_[nn] : 0.f;   // smem copy of b_f
+    float e = rv[c] + bv;
+    e = (svalid && nn < n) ? e : 0.f;
+    jr = fmaf(e, e, jr);
+    rv[c] = 2.f * e;
+  }
+  return jr;
+}
+
+template <int GP, int CBT>
+__global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant__ Params P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the SW128 tiles by pointer arithmetic on the shared array (keeps the shared
+  // address space visible to the compiler: LDS/STS, not generic LD/ST)
+  const uint32_t pad = (1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u;
+  Smem &S = *reinterpret_cast<Smem *>(smem_raw + pad);
+  const Geo &g = P.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int CB = CBT;
+  const uint32_t crank = CB > 1 ? ptx::cluster_ctarank() : 0;
+  const int cid = blockIdx.x / CB, ncl = gridDim.x / CB;
+  const int s0 = (int)crank * MC;   // first sample of this CTA
+  const int T = P.T, n = g.n, k = g.k, m = g.m, mp = P.mp;
+  const bool step = P.mode == 1;
+  // trace: lane 0 of the producers / MMA warp and of epilogue warp 2 record their barrier-wait cycles
+  const bool trec = P.trace != nullptr && lane == 0 && (warp <= 2 || warp == XWARP);
+  const long long t_start = clock64();
+#define TWAIT(IDX, ...)                                                                          \
+  do {                                                                                           \
+    if (trec) {                                                                                  \
+      const long long t0_ = clock64();                                                           \
+      __VA_ARGS__;                                                                               \
+      atomicAdd(&S.tr[IDX], (unsigned long long)(clock64() - t0_));                              \
+    } else {                                                                                     \
+      __VA_ARGS__;                                                                               \
+    }                                                                                            \
+  } while (0)
+
+  // ---- one-time setup
+  if (threadIdx.x < 32) S.tr[threadIdx.x] = 0ull;
+  for (int t = threadIdx.x; t < T * NT; t += NTHREADS) {
+    int ry = t / g.RW, rem = t - ry * g.RW;
+    S.off[t] = (uint16_t)(t < n ? ry * g.W * g.C + rem : 0);
+  }
+  {  // X slots start zeroed: rows past n of the last tile are never written (their products are masked,
+     // but must stay finite)
+    uint4 *z = reinterpret_cast<uint4 *>(S.Xr[0]);
+    for (int t = threadIdx.x; t < (int)(sizeof(S.Xr) + sizeof(S.H) + sizeof(S.D) + sizeof(S.Dl)) / 16; t += NTHREADS)
+      z[t] = make_uint4(0, 0, 0, 0);
+  }
+  for (int t = threadIdx.x; t < 64 * 64; t += NTHREADS) {
+    const int r = t >> 6, c = t & 63;
+    *reinterpret_cast<__nv_bfloat16 *>(S.negI + ptx::sw128_off(r, c)) = __float2bfloat16_rn(r == c ? -1.f : 0.f);
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NW; ++i) { ptx::mbar_init(&S.wfull[i], 1); ptx::mbar_init(&S.wempty[i], 1); }
+    for (int i = 0; i < NX; ++i) { ptx::mbar_init(&S.xfull[i], 1); ptx::mbar_init(&S.xempty[i], 1); }
+    for (int i = 0; i < NP0; ++i) { ptx::mbar_init(&S.p0full[i], 1); ptx::mbar_init(&S.p0empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { ptx::mbar_init(&S.p1full[i], 1); ptx::mbar_init(&S.p1empty[i], 1); }
+    ptx::mbar_init(&S.p0_ok, 1);
+    ptx::mbar_init(&S.u_full, 1);
+    ptx::mbar_init(&S.h_ready, NEPI);
+    ptx::mbar_init(&S.g_full, 1);
+    ptx::mbar_init(&S.d_ready, NEPI);
+    ptx::mbar_init(&S.tmem_free, NEPI);
+    for (int i = 0; i < NRB; ++i) { ptx::mbar_init(&S.r_full[i], 1); ptx::mbar_init(&S.r_empty[i], NEPI); }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&S.dl_full[i], NEPI);
+      ptx::mbar_init(&S.dl_empty[i], 1);
+      ptx::mbar_init(&S.p2_rdx[i], 1);
+      ptx::mbar_init(&S.p2_dw[i], 1);
+      ptx::mbar_init(&S.p2_empty[i], NEPI);
+    }
+    ptx::mbar_init(&S.recv_full, 1);   // armed per tile with expect_tx; completed by the peer's st.async bytes
+    ptx::mbar_init(&S.peer_free, NEPI);
+    ptx::fence_mbar_init();
+  }
+  ptx::fence_proxy_async_smem();   // -I tile is read by the tensor core
+  if (warp == 1) ptx::tmem_alloc<512>(&S.tmem_base);
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (CB > 1) ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tb = S.tmem_base;
+
+  if (warp == 0) {
+    // =================================================================== W producer (TMA)
+    if (lane == 0) {
+      ptx::tma_prefetch(&P.tmW);
+      const uint64_t pol = ptx::policy_evict_first();   // W is streamed once per pass: keep X / dX in L2
+      uint32_t q = 0;
+      const int npass = step ? 3 : 2;
+      for (int f = cid; f < g.F; f += ncl)
+        for (int pass = 0; pass < npass; ++pass)
+          for (int j = 0; j < T; ++j, ++q) {
+            const int s = q % NW;
+            TWAIT(27, ptx::mbar_wait(&S.wempty[s], ((q / NW) & 1) ^ 1));
+            ptx::mbar_arrive_expect_tx(&S.wfull[s], 16384);
+            ptx::tma_load_2d_hint(S.Wr[s], &P.tmW, &S.wfull[s], j * NT, f * KP, pol);
+          }
+    }
+    __syncwarp();
+  } else if (warp == XWARP) {
+    // =================================================================== X producer (cp.async gather)
+    uint32_t q0 = 0, q1 = 0, qx = 0, nf = 0;
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < NXMAP; ++i) ptx::tma_prefetch(&P.tmX[i]);
+    }
+    for (int f = cid; f < g.F; f += ncl, ++nf) {
+      const int fr = f / g.gc, fc = f - fr * g.gc;
+      const int pixbase = (fr * g.s * g.W + fc * g.s) * g.C;
+      // X_j = runs of consecutive image rows (one per receptive-field row): a few TMA boxes per 64-sample half;
+      // the 128B swizzle follows the absolute smem address, so boxes may land at any row of the tile.
+      auto load_tile = [&](uint8_t *dst_tile, uint64_t *bar, int j) {
+        if (lane == 0) {
+          const int rows = min(NT, n - j * NT);
+          ptx::mbar_arrive_expect_tx(bar, (uint32_t)rows * 128u * 2u);
+          const uint32_t *pc = P.xpieces + j * XPMAX;
+          for (int p = 0; p < XPMAX; ++p) {
+            const uint32_t w = __ldg(pc + p);
+            if (w == 0xFFFFFFFFu) break;
+            const int offp = (int)(w & 0xFFFFu), dr = (int)((w >> 16) & 0xFFu), lg = (int)(w >> 24);
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              ptx::tma_load_2d(dst_tile + h * 8192 + dr * 128, &P.tmX[lg], bar, s0 + 64 * h, pixbase + offp);
+          }
+        }
+        __syncwarp();
+      };
+      // pass 0 ring borrows the D'/delta buffers: wait until the previous field is done with them
+      if (step) TWAIT(28, ptx::mbar_wait(&S.p0_ok, (nf & 1) ^ 1));
+      for (int j = 0; j < T; ++j, ++q0) {
+        const int s = q0 % NP0;
+        TWAIT(29, ptx::mbar_wait(&S.p0empty[s], ((q0 / NP0) & 1) ^ 1));
+        load_tile(p0slot(S, s), &S.p0full[s], j);
+      }
+      // pass 1 ring lives in the D' buffer once the encode MMAs are done
+      TWAIT(30, ptx::mbar_wait(&S.u_full, nf & 1));
+      for (int j = 0; j < T; ++j, ++q1) {
+        const int s = q1 & 1;
+        TWAIT(30, ptx::mbar_wait(&S.p1empty[s], ((q1 >> 1) & 1) ^ 1));
+        load_tile(S.D + s * 16384, &S.p1full[s], j);
+      }
+      if (!step) {   // forward: the next field's pass 0 reuses D'; wait until both slots were consumed
+        for (uint32_t qq = q1 - std::min<uint32_t>(q1, 2); qq < q1; ++qq)
+          ptx::mbar_wait(&S.p1empty[qq & 1], (qq >> 1) & 1);
+        continue;
+      }
+      for (int j = 0; j < T; ++j, ++qx) {
+        const int s = qx % NX;
+        TWAIT(31, ptx::mbar_wait(&S.xempty[s], ((qx / NX) & 1) ^ 1));
+        load_tile(S.Xr[s], &S.xfull[s], j);
+      }
+    }
+  } else if (warp == 1) {
+    // =================================================================== MMA issuer
+    if (lane == 0) {
+      const uint32_t id_enc = ptx::idesc_bf16(128, KP, true, false);
+      const uint32_t id_dec = ptx::idesc_bf16(128, NT, false, true);
+      const uint32_t id_nx = ptx::idesc_bf16(128, NT, true, false);   // X^T (-I)
+      const uint32_t id_g = ptx::idesc_bf16(128, KP, false, false);
+      const uint32_t id_dw1 = ptx::idesc_bf16(128, NT, true, true);
+      const uint32_t id_dw2 = ptx::idesc_bf16(128, NT, true, false);
+      const uint32_t sH = ptx::smem_u32(S.H), sD = ptx::smem_u32(S.D), sNI = ptx::smem_u32(S.negI);
+      uint32_t qw = 0, q0 = 0, q1 = 0, qx = 0, nf = 0, ur = 0, ud = 0, u2 = 0;
+      auto wst = [&](uint32_t qq) { return ptx::smem_u32(S.Wr[qq % NW]); };
+      auto wait_w = [&](uint32_t qq) {
+        TWAIT(0, ptx::mbar_wait(&S.wfull[qq % NW], (qq / NW) & 1));
+        ptx::tc_fence_after();
+      };
+      // D = A^T W~_j: A = H' or D' (K-major [128][128]), W~_j MN-major
+      auto mma_aw = [&](uint32_t dcol, uint32_t a_base, uint32_t w_base) {
+#pragma unroll
+        for (int kk = 0; kk < KP / 16; ++kk) {
+          uint64_t ad = ptx::sdesc_sw128(a_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+          uint64_t bd = ptx::sdesc_sw128(w_base + kk * 2048, 16384, 1024);
+          ptx::umma_bf16(tb + dcol, ad, bd, id_dec, kk > 0);
+        }
+      };
+      // D += X_j^T (-I): subtracts the patch values exactly (X_j MN-major A, -I K-major B)
+      auto mma_negx = [&](uint32_t dcol, uint32_t x_base) {
+#pragma unroll
+        for (int kk = 0; kk < NT / 16; ++kk) {
+          uint64_t ad = ptx::sdesc_sw128(x_base + kk * 2048, 8192, 1024);
+          uint64_t bd = ptx::sdesc_sw128(sNI + kk * 32, 16, 1024);
+          ptx::umma_bf16(tb + dcol, ad, bd, id_nx, 1);
+        }
+      };
+      for (int f = cid; f < g.F; f += ncl, ++nf) {
+        TWAIT(2, ptx::mbar_wait(&S.tmem_free, (nf & 1) ^ 1));
+        ptx::tc_fence_after();
+        // ---- pass 0: U^T = X^T W~^T
+        for (int j = 0; j < T; ++j, ++qw, ++q0) {
+          wait_w(qw);
+          TWAIT(1, ptx::mbar_wait(&S.p0full[q0 % NP0], (q0 / NP0) & 1));
+          ptx::tc_fence_after();
+          ptx::fence_proxy_async_smem();
+          const uint32_t xs = ptx::smem_u32(p0slot(S, q0 % NP0));
+#pragma unroll
+          for (int kk = 0; kk < NT / 16; ++kk) {
+            uint64_t ad = ptx::sdesc_sw128(xs + kk * 2048, 8192, 1024);
+            uint64_t bd = ptx::sdesc_sw128(wst(qw) + kk * 32, 16, 1024);
+            ptx::umma_bf16(tb + 0, ad, bd, id_enc, (j | kk) != 0);
+          }
+          ptx::umma_commit(&S.wempty[qw % NW]);
+          ptx::umma_commit(&S.p0empty[q0 % NP0]);
+        }
+        ptx::umma_commit(&S.u_full);
+        // ---- pass 1: R_j - X_j, then G += delta_{j-GLAG} W~_{j-GLAG}^T
+        TWAIT(3, ptx::mbar_wait(&S.h_ready, nf & 1));
+        ptx::tc_fence_after();
+        ptx::fence_proxy_async_smem();
+        const uint32_t qw1 = qw;
+        auto issue_G = [&](int j) {
+          const uint32_t qj = qw1 + j, db_ = ud & 1;
+          TWAIT(5, ptx::mbar_wait(&S.dl_full[db_], (ud >> 1) & 1));
+          ptx::tc_fence_after();
+          ptx::fence_proxy_async_smem();
+          const uint32_t dl = ptx::smem_u32(S.Dl[db_]);
+#pragma unroll
+          for (int kk = 0; kk < NT / 16; ++kk) {
+            uint64_t ad = ptx::sdesc_sw128(dl + kk * 32, 16, 1024);
+            uint64_t bd = ptx::sdesc_sw128(wst(qj) + kk * 32, 16, 1024);
+            ptx::umma_bf16(tb + 384, ad, bd, id_g, (j | kk) != 0);
+          }
+          ptx::umma_commit(&S.dl_empty[db_]);
+          ptx::umma_commit(&S.wempty[qj % NW]);
+          ++ud;
+        };
+        for (int j = 0; j < T; ++j, ++qw, ++ur, ++q1) {
+          wait_w(qw);
+          const uint32_t rb = ur % NRB, s1 = q1 & 1;
+          TWAIT(4, ptx::mbar_wait(&S.r_empty[rb], ((ur / NRB) & 1) ^ 1));
+          TWAIT(1, ptx::mbar_wait(&S.p1full[s1], (q1 >> 1) & 1));
+          ptx::tc_fence_after();
+          ptx::fence_proxy_async_smem();
+          mma_aw(128 + 64 * rb, sH, wst(qw));
+          mma_negx(128 + 64 * rb, sD + s1 * 16384);
+          ptx::umma_commit(&S.r_full[rb]);
+          ptx::umma_commit(&S.p1empty[s1]);
+          if (step) {
+            if (j >= GLAG) issue_G(j - GLAG);
+          } else {
+            ptx::umma_commit(&S.wempty[qw % NW]);
+          }
+        }
+        if (!step) continue;
+        for (int j = std::max(0, T - GLAG); j < T; ++j) issue_G(j);
+        ptx::umma_commit(&S.g_full);
+        // ---- pass 2: R_j - X_j and dX_j (W stage released), then dW_j one tile behind
+        TWAIT(6, ptx::mbar_wait(&S.d_ready, nf & 1));
+        ptx::tc_fence_after();
+        ptx::fence_proxy_async_smem();
+        const uint32_t u2_0 = u2, qx0 = qx;
+        auto issue_dW = [&](int j) {
+          const uint32_t pb = (u2_0 + j) & 1, db_ = ud & 1, xsl = (qx0 + j) % NX;
+          TWAIT(8, ptx::mbar_wait(&S.dl_full[db_], (ud >> 1) & 1));
+          ptx::tc_fence_after();
+          ptx::fence_proxy_async_smem();
+          const uint32_t dl = ptx::smem_u32(S.Dl[db_]), dcol = 192 * pb + 128, xs = ptx::smem_u32(S.Xr[xsl]);
+#pragma unroll
+          for (int kk = 0; kk < MC / 16; ++kk) {   // H' delta_j^T  (K = samples)
+            uint64_t ad = ptx::sdesc_sw128(sH + kk * 2048, 16384, 1024);
+            uint64_t bd = ptx::sdesc_sw128(dl + kk * 2048, 16384, 1024);
+            ptx::umma_bf16(tb + dcol, ad, bd, id_dw1, kk > 0);
+          }
+#pragma unroll
+          for (int kk = 0; kk < MC / 16; ++kk) {   // + D' X_j^T
+            uint64_t ad = ptx::sdesc_sw128(sD + kk * 2048, 16384, 1024);
+            uint64_t bd = ptx::sdesc_sw128(xs + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
+            ptx::umma_bf16(tb + dcol, ad, bd, id_dw2, 1);
+          }
+          ptx::umma_commit(&S.p2_dw[pb]);
+          ptx::umma_commit(&S.dl_empty[db_]);
+          ptx::umma_commit(&S.xempty[xsl]);
+          ++ud;
+        };
+        for (int j = 0; j < T; ++j, ++qw, ++u2, ++qx) {
+          wait_w(qw);
+          const uint32_t pb = u2 & 1, xsl = qx % NX;
+          TWAIT(9, ptx::mbar_wait(&S.xfull[xsl], (qx / NX) & 1));
+          TWAIT(7, ptx::mbar_wait(&S.p2_empty[pb], ((u2 >> 1) & 1) ^ 1));
+          ptx::tc_fence_after();
+          ptx::fence_proxy_async_smem();
+          mma_aw(192 * pb, sH, wst(qw));                    // R^T_j
+          mma_negx(192 * pb, ptx::smem_u32(S.Xr[xsl]));     //   - X_j^T
+          mma_aw(192 * pb + 64, sD, wst(qw));               // dX^T_j (alpha folded into D')
+          ptx::umma_commit(&S.p2_rdx[pb]);
+          ptx::umma_commit(&S.wempty[qw % NW]);
+          if (j > 0) issue_dW(j - 1);
+        }
+        issue_dW(T - 1);
+        ptx::umma_commit(&S.p0_ok);   // D', delta and the X ring are free for the next field's pass 0
+      }
+    }
+    __syncwarp();
+  } else {
+    // =================================================================== epilogue (warps 2..9)
+    const int qd = warp & 3;              // TMEM lane quarter
+    const int ew = warp - 2;              // epilogue warp index 0..7
+    const int half = ew >> 2;             // column half of every 64-column tile (and of the 128 filters)
+    const int etid = threadIdx.x - 64;    // 0..255
+    const int row = qd * 32 + lane;       // TMEM lane: sample (U, R, G, dX) or filter row (dW)
+    const uint32_t tl = tb + ((uint32_t)(qd * 32) << 16);
+    const int gi = s0 + row;              // global sample index
+    const bool svalid = gi < m;
+    const int ng = k / GP;
+    const int hc = 32 * half;             // first column of this warp within a tile
+    uint32_t nf = 0, ur = 0, ud = 0, u2 = 0;
+    for (int f = cid; f < g.F; f += ncl, ++nf) {
+      const int fr = f / g.gc, fc = f - fr * g.gc;
+      const int64_t pixbase = ((int64_t)fr * g.s * g.W + (int64_t)fc * g.s) * g.C;
+      ptx::named_bar_sync(1, 32 * NEPI);
+      if (etid < KP) S.sig[etid] = etid < k ? P.sigma[(int64_t)f * k + etid] : 1.f;
+      for (int t = etid; t < n; t += 32 * NEPI) S.bs[t] = P.b[(int64_t)f * n + t];
+      ptx::named_bar_sync(1, 32 * NEPI);
+      const float a = P.alpha[f];
+      const float *bf_ = S.bs;
+      double jr = 0.0, js = 0.0;
+      float dap = 0.f, rsq = 0.f;
+      // ------------------------------------------------ E0: pooling / sparsity, H' (filters [64 half, +64))
+      TWAIT(11, ptx::mbar_wait(&S.u_full, nf & 1));
+      ptx::tc_fence_after();
+#pragma unroll 1
+      for (int cc = 2 * half; cc < 2 * half + 2; ++cc) {
+        float u[32];
+        ptx::tmem_ld16(tl + cc * 32, u);
+        ptx::tmem_ld16(tl + cc * 32 + 16, u + 16);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int t = 0; t < 32; ++t) u[t] *= S.sig[cc * 32 + t];
+#pragma unroll
+        for (int G0 = 0; G0 < 32; G0 += GP) {
+          float ss = 0.f;
+#pragma unroll
+          for (int t = 0; t < GP; ++t) { float h = a * u[G0 + t]; ss = fmaf(h, h, ss); }
+          const int G = (cc * 32 + G0) / GP;
+          if (G < ng && svalid) {
+            float sG = sqrtf(P.eps + ss);
+            js += (double)sG;
+            if (P.want_pooled) P.pooled[(((int64_t)gi * g.gr + fr) * g.gc + fc) * ng + G] = sG;
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 32; ++t) u[t] = svalid ? S.sig[cc * 32 + t] * a * u[t] : 0.f;
+        uint8_t *blk = S.H + (cc >> 1) * 16384;
+#pragma unroll
+        for (int t = 0; t < 32; t += 8) st8(blk, row, (cc & 1) * 32 + t, u + t);
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&S.h_ready);
+      // ------------------------------------------------ E1: residual, delta, db (pass 1)
+#pragma unroll 1
+      for (int j = 0; j < T; ++j, ++ur) {
+        const uint32_t rb = ur % NRB;
+        TWAIT(12, ptx::mbar_wait(&S.r_full[rb], (ur / NRB) & 1));
+        ptx::tc_fence_after();
+        float rv[32];
+        ptx::tmem_ld16(tl + 128 + 64 * rb + hc, rv);
+        ptx::tmem_ld16(tl + 128 + 64 * rb + hc + 16, rv + 16);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&S.r_empty[rb]);
+        jr += (double)residual32(rv, j * NT + hc, n, bf_, svalid);
+        if (step) {
+          const uint32_t db_ = ud & 1;
+          TWAIT(14, ptx::mbar_wait(&S.dl_empty[db_], ((ud >> 1) & 1) ^ 1));
+#pragma unroll
+          for (int c = 0; c < 32; c += 8) st8(S.Dl[db_], row, hc + c, rv + c);
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&S.dl_full[db_]);
+          ++ud;
+          // db partial: column sums over this warp's 32 samples (butterfly transpose-reduce: lane l <- column l)
+#pragma unroll
+          for (int o = 16, w = 16; o >= 1; o >>= 1, w >>= 1) {
+            const bool up = lane & o;
+#pragma unroll
+            for (int t = 0; t < w; ++t) {
+              float send = up ? rv[t] : rv[t + w];
+              float keep = up ? rv[t + w] : rv[t];
+              rv[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+          }
+          S.dbw[j & 1][ew][lane] = rv[0];
+          ptx::named_bar_sync(1, 32 * NEPI);
+          if ((ew & 3) == 0) {
+            const int nn = j * NT + hc + lane;
+            const float sdb = S.dbw[j & 1][ew][lane] + S.dbw[j & 1][ew + 1][lane] + S.dbw[j & 1][ew + 2][lane] +
+                              S.dbw[j & 1][ew + 3][lane];
+            if (nn < n) P.db_part[((int64_t)f * CB + crank) * n + nn] = sdb;
+          }
+        }
+      }
+      if (step) {
+        // ---------------------------------------------- E1b: D = sigma.G~ + lambda h/s, dalpha, D'
+        TWAIT(16, ptx::mbar_wait(&S.g_full, nf & 1));
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int cc = 2 * half; cc < 2 * half + 2; ++cc) {
+          float u[32], gg[32];
+          ptx::tmem_ld16(tl + cc * 32, u);
+          ptx::tmem_ld16(tl + cc * 32 + 16, u + 16);
+          ptx::tmem_ld16(tl + 384 + cc * 32, gg);
+          ptx::tmem_ld16(tl + 384 + cc * 32 + 16, gg + 16);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int t = 0; t < 32; ++t) u[t] *= S.sig[cc * 32 + t];
+#pragma unroll
+          for (int G0 = 0; G0 < 32; G0 += GP) {
+            float ss = 0.f;
+#pragma unroll
+            for (int t = 0; t < GP; ++t) { float h = a * u[G0 + t]; ss = fmaf(h, h, ss); }
+            const float sG = sqrtf(P.eps + ss);
+            const float inv = sG > 0.f ? P.lam / sG : 0.f;
+#pragma unroll
+            for (int t = 0; t < GP; ++t) {
+              const int col = cc * 32 + G0 + t;
+              float Dv = fmaf(S.sig[col], gg[G0 + t], a * u[G0 + t] * inv);
+              Dv = (svalid && col < k) ? Dv : 0.f;
+              dap = fmaf(Dv, u[G0 + t], dap);
+              gg[G0 + t] = S.sig[col] * a * Dv;   // D'
+            }
+          }
+          uint8_t *blk = S.D + (cc >> 1) * 16384;
+#pragma unroll
+          for (int t = 0; t < 32; t += 8) st8(blk, row, (cc & 1) * 32 + t, gg + t);
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&S.d_ready);
+        // ---------------------------------------------- E2: dX, dW, fused projected SGD (pass 2)
+        const float sg_r = S.sig[row];
+        const uint64_t pol_ef = ptx::policy_evict_first();   // W~ master / shadow streams
+        const float inv_sg = 1.f / sg_r;
+#pragma unroll 1
+        for (int j = 0; j < T; ++j, ++u2) {
+          const uint32_t pb = u2 & 1, base = 192 * pb;
+          TWAIT(18, ptx::mbar_wait(&S.p2_rdx[pb], (u2 >> 1) & 1));
+          ptx::tc_fence_after();
+          float rv[32];
+          ptx::tmem_ld16(tl + base + hc, rv);
+          ptx::tmem_ld16(tl + base + hc + 16, rv + 16);
+          ptx::tmem_ld_wait();
+          residual32(rv, j * NT + hc, n, bf_, svalid);
+          {
+            const uint32_t db_ = ud & 1;
+            TWAIT(20, ptx::mbar_wait(&S.dl_empty[db_], ((ud >> 1) & 1) ^ 1));
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) st8(S.Dl[db_], row, hc + c, rv + c);
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&S.dl_full[db_]);
+            ++ud;
+          }
+          // dx = alpha W^T D - delta, overlap-added into the image gradient with 16-byte reductions:
+          // 4x4 lane transposes give each lane 4 consecutive samples of one column.
+          {
+            const int r4 = lane & 3;
+            const bool o1 = r4 & 1, o2 = r4 & 2;
+            float *dcol = P.dxt + pixbase * mp + (s0 + qd * 32 + (lane & ~3));
+            const bool grp_ok = s0 + qd * 32 + (lane & ~3) < mp;
+#pragma unroll
+            for (int blk = 0; blk < 8; ++blk) {
+              if ((blk & 1) == 0) {   // TMEM loads in 8-column pieces keep the register footprint small
+                float t8[8];
+                ptx::tmem_ld8(tl + base + 64 + hc + 4 * blk, t8);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int q = 0; q < 8; ++q) rv[4 * blk + q] = t8[q] - rv[4 * blk + q];   // rv <- dx
+              }
+              float a0 = rv[4 * blk], a1 = rv[4 * blk + 1], a2 = rv[4 * blk + 2], a3 = rv[4 * blk + 3];
+              float t0 = __shfl_xor_sync(0xffffffffu, o1 ? a0 : a1, 1);
+              float t1 = __shfl_xor_sync(0xffffffffu, o1 ? a2 : a3, 1);
+              if (o1) { a0 = t0; a2 = t1; } else { a1 = t0; a3 = t1; }
+              t0 = __shfl_xor_sync(0xffffffffu, o2 ? a0 : a2, 2);
+              t1 = __shfl_xor_sync(0xffffffffu, o2 ? a1 : a3, 2);
+              if (o2) { a0 = t0; a1 = t1; } else { a2 = t0; a3 = t1; }
+              const int nn = j * NT + hc + 4 * blk + r4;
+              if (nn < n && grp_ok) red_v4(dcol + (int64_t)S.off[nn] * mp, a0, a1, a2, a3);
+            }
+          }
+          // dW_j (lanes = filter rows, this warp's 32 columns): prefetch the owned W~ run, sum the batch slices
+          // over the cluster, then projected SGD. CTA c owns the 16-column chunk [16c, 16c+16) of each half.
+          constexpr int NC = CB > 1 ? 16 : 32, NV = NC / 4;
+          const int oc = CB > 1 ? 16 * (int)crank : 0;
+          const int c0 = j * NT + hc + oc;   // multiple of 16: 64-byte aligned in the padded rows
+          float4 wv[NV];
+          float *wr = P.W + ((int64_t)f * k + min(row, k - 1)) * P.wp + c0;
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+            wv[v] = (c0 + 4 * v < P.wp) ? ptx::ld_f4_ef(wr + 4 * v, pol_ef) : make_float4(0, 0, 0, 0);
+          TWAIT(21, ptx::mbar_wait(&S.p2_dw[pb], (u2 >> 1) & 1));
+          ptx::tc_fence_after();
+          float dw[32];
+          ptx::tmem_ld16(tl + base + 128 + hc, dw);
+          ptx::tmem_ld16(tl + base + 128 + hc + 16, dw + 16);
+          ptx::tmem_ld_wait();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&S.p2_empty[pb]);   // TMEM buffer pb fully read by this warp
+          if (CB > 1) {
+            if (crank) {   // owned chunk to dw[0..15], the peer's chunk to dw[16..31]
+#pragma unroll
+              for (int t = 0; t < 16; ++t) { float tmp = dw[t]; dw[t] = dw[t + 16]; dw[t + 16] = tmp; }
+            }
+            const uint32_t peer = crank ^ 1u;
+            // arm this tile's receive phase: 8 warps x 32 rows x 16 floats arrive from the peer via st.async
+            if (etid == 0) ptx::mbar_arrive_expect_tx(&S.recv_full, 2 * 128 * 16 * 4);
+            TWAIT(22, ptx::mbar_wait(&S.peer_free, (u2 & 1) ^ 1));
+            const uint32_t rdst = ptx::mapa(ptx::smem_u32(&S.recv[half][row][0]), peer);
+            const uint32_t rbar = ptx::mapa(ptx::smem_u32(&S.recv_full), peer);
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              ptx::st_async_v4(rdst + 16 * t, make_float4(dw[16 + 4 * t], dw[17 + 4 * t], dw[18 + 4 * t], dw[19 + 4 * t]),
+                               rbar);
+            TWAIT(22, ptx::mbar_wait(&S.recv_full, u2 & 1));
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float4 r4 = *reinterpret_cast<const float4 *>(&S.recv[half][row][4 * t]);
+              dw[4 * t] += r4.x;
+              dw[4 * t + 1] += r4.y;
+              dw[4 * t + 2] += r4.z;
+              dw[4 * t + 3] += r4.w;
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_remote_relaxed(ptx::mapa(ptx::smem_u32(&S.peer_free), peer));
+          }
+          if (row < k) {
+            float4 vv[NV];
+            if (P.vW) {
+              const float *vr = P.vW + ((int64_t)f * k + row) * P.wp + c0;
+#pragma unroll
+              for (int v = 0; v < NV; ++v)
+                vv[v] = (c0 + 4 * v < P.wp) ? *reinterpret_cast<const float4 *>(vr + 4 * v) : make_float4(0, 0, 0, 0);
+            }
+            float wn[NC];
+#pragma unroll
+            for (int t = 0; t < NC; ++t) {
+              const float d = (c0 + t < n) ? dw[t] * inv_sg : 0.f;   // accumulator holds sigma_r * dJ/dW
+              dw[t] = d;
+              float upd = -P.lr * d;
+              if (P.vW) {
+                float vo = (&vv[t >> 2].x)[t & 3];
+                upd = fmaf(P.mu, vo, upd);
+                (&vv[t >> 2].x)[t & 3] = upd;
+              }
+              wn[t] = fmaf(sg_r, (&wv[t >> 2].x)[t & 3], upd);
+              rsq = fmaf(wn[t], wn[t], rsq);
+            }
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+              if (c0 + 4 * v < P.wp)
+                ptx::st_f4_ef(wr + 4 * v, make_float4(wn[4 * v], wn[4 * v + 1], wn[4 * v + 2], wn[4 * v + 3]), pol_ef);
+            __nv_bfloat16 *br = P.Wb + ((int64_t)f * KP + row) * P.n_al + c0;
+#pragma unroll
+            for (int v = 0; v < NC / 8; ++v)
+              if (c0 + 8 * v < P.n_al) {
+                uint4 q4;
+                q4.x = ptx::pack_bf16x2(wn[8 * v], wn[8 * v + 1]);
+                q4.y = ptx::pack_bf16x2(wn[8 * v + 2], wn[8 * v + 3]);
+                q4.z = ptx::pack_bf16x2(wn[8 * v + 4], wn[8 * v + 5]);
+                q4.w = ptx::pack_bf16x2(wn[8 * v + 6], wn[8 * v + 7]);
+                ptx::st_u4_ef(br + 8 * v, q4, pol_ef);
+              }
+            if (P.vW) {
+              float *vr = P.vW + ((int64_t)f * k + row) * P.wp + c0;
+#pragma unroll
+              for (int v = 0; v < NV; ++v)
+                if (c0 + 4 * v < P.wp) *reinterpret_cast<float4 *>(vr + 4 * v) = vv[v];
+            }
+            if (P.keep_grads) {
+              float *gr = P.gW + ((int64_t)f * k + row) * P.wp + c0;
+#pragma unroll
+              for (int v = 0; v < NV; ++v)
+                if (c0 + 4 * v < P.wp)
+                  *reinterpret_cast<float4 *>(gr + 4 * v) = make_float4(dw[4 * v], dw[4 * v + 1], dw[4 * v + 2], dw[4 * v + 3]);
+            }
+          }
+        }
+      }
+      // ------------------------------------------------ per-field partial sums (fixed order)
+      jr = warp_sum(jr);
+      js = warp_sum(js);
+      dap = warp_sum(dap);
+      if (lane == 0) { S.redd[ew][0] = jr; S.redd[ew][1] = js; S.redf[ew] = dap; }
+      ptx::named_bar_sync(1, 32 * NEPI);
+      if (etid == 0) {
+        double a0 = 0.0, a1 = 0.0;
+        float a2 = 0.f;
+        for (int w = 0; w < NEPI; ++w) { a0 += S.redd[w][0]; a1 += S.redd[w][1]; a2 += S.redf[w]; }
+        P.loss_part[((int64_t)f * CB + crank) * 2 + 0] = a0;
+        P.loss_part[((int64_t)f * CB + crank) * 2 + 1] = (double)P.lam * a1;
+        P.da_part[(int64_t)f * CB + crank] = a2;
+      }
+      if (step) P.rowsq_part[(((int64_t)f * CB + crank) * 2 + half) * KP + row] = rsq;
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&S.tmem_free);
+    }
+  }
+  // ---- teardown
+  if (trec) atomicAdd(&S.tr[warp == 1 ? 10 : warp == 0 ? 25 : warp == XWARP ? 24 : 26],
+                      (unsigned long long)(clock64() - t_start));
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (P.trace && threadIdx.x < 32) atomicAdd(&P.trace[threadIdx.x], S.tr[threadIdx.x]);
+#undef TWAIT
+  if (CB > 1) ptx::cluster_sync();
+  if (warp == 1) ptx::tmem_dealloc<512>(tb);
+}
+
+}  // namespace tc
+}  // namespace lcae

@@ -1,0 +1,48 @@
+"""Dev tool: per-role barrier-wait breakdown of the fused step kernel (lcae_dev_trace).
+usage: python tools/trace_step.py [c3|c2] [steps]"""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+from paper_1502_03409_b200 import lcae  # noqa: E402
+from paper_1502_03409_b200.inputs import CONFIGS, make_images, make_params  # noqa: E402
+
+NAMES = {0: "mma:wfull", 1: "mma:p0full", 2: "mma:tmem_free", 3: "mma:h_ready", 4: "mma:r_empty",
+         5: "mma:dl_full(G)", 6: "mma:d_ready", 7: "mma:p2_empty", 8: "mma:dl_full(dW)", 9: "mma:xfull(dW)",
+         10: "mma:TOTAL", 11: "epi:u_full", 12: "epi:r_full", 13: "epi:p1full", 14: "epi:dl_empty(E1)",
+         16: "epi:g_full", 18: "epi:p2_rdx", 19: "epi:xfull", 20: "epi:dl_empty(E2)", 21: "epi:p2_dw",
+         22: "epi:dsmem", 24: "xprod:TOTAL", 25: "wprod:TOTAL", 26: "epi:TOTAL", 27: "wprod:wempty",
+         28: "xprod:p0_ok", 29: "xprod:p0empty", 30: "xprod:p1", 31: "xprod:xempty"}
+
+cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c3"
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+shape = CONFIGS[cfg_name]
+lib = lcae.lib
+lib.lcae_dev_trace.restype = C.c_int
+lib.lcae_dev_trace.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+L = lcae.Layer(lcae.make_config(shape, precision=lcae.BF16))
+W, a, b = make_params(shape, seed=0)
+L.set_params(W, a, b)
+x = torch.from_numpy(make_images(shape, seed=1)).cuda()
+for _ in range(2):
+    L.step(x, None, want_loss=False)
+torch.cuda.synchronize()
+lcae.check(lib.lcae_dev_trace(L.h, 1, None))
+L.profile(True)
+for _ in range(steps):
+    L.step(x, None, want_loss=False)
+torch.cuda.synchronize()
+ms, nl = L.profile_read()
+out = (C.c_ulonglong * 32)()
+lcae.check(lib.lcae_dev_trace(L.h, 0, out))
+ctas = min(shape.fields * ((shape.batch + 127) // 128), 148 // ((shape.batch + 127) // 128) * ((shape.batch + 127) // 128))
+per = lambda v: v / ctas / steps  # noqa: E731
+tot = per(out[10])
+print(f"{cfg_name}: kernel {ms / nl:.3f} ms/launch; per-CTA cycles per step (mma total {tot:.0f})")
+for i in sorted(NAMES):
+    if out[i]:
+        print(f"  {NAMES[i]:20s} {per(out[i]):14.0f}  {100 * per(out[i]) / tot:6.1f}%")
