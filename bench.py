@@ -159,14 +159,15 @@ def run_ours(args, shape):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
+    stream = torch.cuda.Stream()
+    pk = peaks()
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_1502_03409_b200 import parallel
         tile = parallel.plan(shape, world)[rank]
-        runner = parallel.TileRunner(shape, tile, world, rank)
-    stream = torch.cuda.Stream()
-    pk = peaks()
+        with torch.cuda.stream(stream):
+            runner = parallel.TileRunner(shape, tile, world, rank, stream=stream.cuda_stream)
     with torch.cuda.stream(stream):
         if world == 1:
             cfg = lcae.make_config(shape, precision=lcae.BF16, stream=stream.cuda_stream)
