@@ -229,6 +229,12 @@ def run_ours(args, shape):
     kern_avg = kern_ms / max(1, kern_n)
     per_kernel_flops = flops / world
     achieved = per_kernel_flops / (kern_avg * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            traffic = json.load(fh).get(shape.name, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -240,7 +246,7 @@ def run_ours(args, shape):
                    "l2": "working set > L2 (fp32 W master 4 B/param streamed every step)"},
         "tflops": flops / (ms_step * 1e-3) / 1e12,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
-                     "frac": achieved / pk["bf16_sus"], "traffic": None,
+                     "frac": achieved / pk["bf16_sus"], "traffic": traffic,
                      "kernel": "lcae::tc::step_kernel", "kernel_ms": kern_avg,
                      "peak_source": f"{pk['src']} bf16_tflops_sustained (kernel timed inside a long step)"},
         "gpu_launches": launches_per_step * args.steps,

@@ -213,7 +213,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             const int s = q % NW;
             TWAIT(27, ptx::mbar_wait(&S.wempty[s], ((q / NW) & 1) ^ 1));
             ptx::mbar_arrive_expect_tx(&S.wfull[s], 16384);
-            ptx::tma_load_2d_hint(S.Wr[s], &P.tmW, &S.wfull[s], j * NT, f * KP, pol);
+            if (pass == npass - 1)   // last read of W~_f this step: evict first; earlier passes keep it in L2
+              ptx::tma_load_2d_hint(S.Wr[s], &P.tmW, &S.wfull[s], j * NT, f * KP, pol);
+            else
+              ptx::tma_load_2d(S.Wr[s], &P.tmW, &S.wfull[s], j * NT, f * KP);
           }
     }
     __syncwarp();
