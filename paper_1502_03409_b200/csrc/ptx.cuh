@@ -109,13 +109,23 @@ __device__ __forceinline__ float4 ld_f4_ef(const float *p, uint64_t pol) {
 }
 __device__ __forceinline__ void st_f4_ef(float *p, float4 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
-               "f"(v.w), "l"(pol)
-               : "memory");
+               "f"(v.w), "l"(pol));
 }
 __device__ __forceinline__ void st_u4_ef(void *p, uint4 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w), "l"(pol)
+               "r"(v.w), "l"(pol));
+}
+
+// Plain (non-tensor) bulk copy global -> shared completing on an mbarrier (bytes multiple of 16).
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+// Make this thread's generic-proxy global writes visible to later async-proxy (TMA / bulk) reads.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- fences

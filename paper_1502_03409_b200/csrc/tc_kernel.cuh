@@ -93,6 +93,9 @@ struct __align__(1024) Smem {
   unsigned long long tr[32];   // optional wait-cycle trace (lcae_dev_trace)
 };
 
+#define UMMA_E(...) do { if (ptx::elect_one()) ptx::umma_bf16(__VA_ARGS__); __syncwarp(); } while (0)
+#define UCOMMIT_E(bar) do { if (ptx::elect_one()) ptx::umma_commit(bar); __syncwarp(); } while (0)
+
 __device__ __forceinline__ uint8_t *p0slot(Smem &S, int i) { return i < 2 ? S.D + i * 16384 : S.Dl[i - 2]; }
 
 // store 8 consecutive bf16 (cols c0..c0+7 of row `row`) into a [rows][64] SW128 block
@@ -275,7 +278,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     }
   } else if (warp == 1) {
     // =================================================================== MMA issuer
-    if (lane == 0) {
+    {   // warp-uniform: every lane walks the schedule, one elected lane issues (2x the single-lane MMA rate)
       const uint32_t id_enc = ptx::idesc_bf16(128, KP, true, false);
       const uint32_t id_dec = ptx::idesc_bf16(128, NT, false, true);
       const uint32_t id_nx = ptx::idesc_bf16(128, NT, true, false);   // X^T (-I)
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         for (int kk = 0; kk < KP / 16; ++kk) {
           uint64_t ad = ptx::sdesc_sw128(a_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
           uint64_t bd = ptx::sdesc_sw128(w_base + kk * 2048, 16384, 1024);
-          ptx::umma_bf16(tb + dcol, ad, bd, id_dec, kk > 0);
+          UMMA_E(tb + dcol, ad, bd, id_dec, kk > 0);
         }
       };
       // D += X_j^T (-I): subtracts the patch values exactly (X_j MN-major A, -I K-major B)
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         for (int kk = 0; kk < NT / 16; ++kk) {
           uint64_t ad = ptx::sdesc_sw128(x_base + kk * 2048, 8192, 1024);
           uint64_t bd = ptx::sdesc_sw128(sNI + kk * 32, 16, 1024);
-          ptx::umma_bf16(tb + dcol, ad, bd, id_nx, 1);
+          UMMA_E(tb + dcol, ad, bd, id_nx, 1);
         }
       };
       for (int f = cid; f < g.F; f += ncl, ++nf) {
@@ -321,12 +324,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           for (int kk = 0; kk < NT / 16; ++kk) {
             uint64_t ad = ptx::sdesc_sw128(xs + kk * 2048, 8192, 1024);
             uint64_t bd = ptx::sdesc_sw128(wst(qw) + kk * 32, 16, 1024);
-            ptx::umma_bf16(tb + 0, ad, bd, id_enc, (j | kk) != 0);
+            UMMA_E(tb + 0, ad, bd, id_enc, (j | kk) != 0);
           }
-          ptx::umma_commit(&S.wempty[qw % NW]);
-          ptx::umma_commit(&S.p0empty[q0 % NP0]);
+          UCOMMIT_E(&S.wempty[qw % NW]);
+          UCOMMIT_E(&S.p0empty[q0 % NP0]);
         }
-        ptx::umma_commit(&S.u_full);
+        UCOMMIT_E(&S.u_full);
         // ---- pass 1: R_j - X_j, then G += delta_{j-GLAG} W~_{j-GLAG}^T
         TWAIT(3, ptx::mbar_wait(&S.h_ready, nf & 1));
         ptx::tc_fence_after();
@@ -342,10 +345,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           for (int kk = 0; kk < NT / 16; ++kk) {
             uint64_t ad = ptx::sdesc_sw128(dl + kk * 32, 16, 1024);
             uint64_t bd = ptx::sdesc_sw128(wst(qj) + kk * 32, 16, 1024);
-            ptx::umma_bf16(tb + 384, ad, bd, id_g, (j | kk) != 0);
+            UMMA_E(tb + 384, ad, bd, id_g, (j | kk) != 0);
           }
-          ptx::umma_commit(&S.dl_empty[db_]);
-          ptx::umma_commit(&S.wempty[qj % NW]);
+          UCOMMIT_E(&S.dl_empty[db_]);
+          UCOMMIT_E(&S.wempty[qj % NW]);
           ++ud;
         };
         for (int j = 0; j < T; ++j, ++qw, ++ur, ++q1) {
@@ -357,17 +360,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           ptx::fence_proxy_async_smem();
           mma_aw(128 + 64 * rb, sH, wst(qw));
           mma_negx(128 + 64 * rb, sD + s1 * 16384);
-          ptx::umma_commit(&S.r_full[rb]);
-          ptx::umma_commit(&S.p1empty[s1]);
+          UCOMMIT_E(&S.r_full[rb]);
+          UCOMMIT_E(&S.p1empty[s1]);
           if (step) {
             if (j >= GLAG) issue_G(j - GLAG);
           } else {
-            ptx::umma_commit(&S.wempty[qw % NW]);
+            UCOMMIT_E(&S.wempty[qw % NW]);
           }
         }
         if (!step) continue;
         for (int j = std::max(0, T - GLAG); j < T; ++j) issue_G(j);
-        ptx::umma_commit(&S.g_full);
+        UCOMMIT_E(&S.g_full);
         // ---- pass 2: R_j - X_j and dX_j (W stage released), then dW_j one tile behind
         TWAIT(6, ptx::mbar_wait(&S.d_ready, nf & 1));
         ptx::tc_fence_after();
@@ -383,17 +386,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           for (int kk = 0; kk < MC / 16; ++kk) {   // H' delta_j^T  (K = samples)
             uint64_t ad = ptx::sdesc_sw128(sH + kk * 2048, 16384, 1024);
             uint64_t bd = ptx::sdesc_sw128(dl + kk * 2048, 16384, 1024);
-            ptx::umma_bf16(tb + dcol, ad, bd, id_dw1, kk > 0);
+            UMMA_E(tb + dcol, ad, bd, id_dw1, kk > 0);
           }
 #pragma unroll
           for (int kk = 0; kk < MC / 16; ++kk) {   // + D' X_j^T
             uint64_t ad = ptx::sdesc_sw128(sD + kk * 2048, 16384, 1024);
             uint64_t bd = ptx::sdesc_sw128(xs + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
-            ptx::umma_bf16(tb + dcol, ad, bd, id_dw2, 1);
+            UMMA_E(tb + dcol, ad, bd, id_dw2, 1);
           }
-          ptx::umma_commit(&S.p2_dw[pb]);
-          ptx::umma_commit(&S.dl_empty[db_]);
-          ptx::umma_commit(&S.xempty[xsl]);
+          UCOMMIT_E(&S.p2_dw[pb]);
+          UCOMMIT_E(&S.dl_empty[db_]);
+          UCOMMIT_E(&S.xempty[xsl]);
           ++ud;
         };
         for (int j = 0; j < T; ++j, ++qw, ++u2, ++qx) {
@@ -406,12 +409,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           mma_aw(192 * pb, sH, wst(qw));                    // R^T_j
           mma_negx(192 * pb, ptx::smem_u32(S.Xr[xsl]));     //   - X_j^T
           mma_aw(192 * pb + 64, sD, wst(qw));               // dX^T_j (alpha folded into D')
-          ptx::umma_commit(&S.p2_rdx[pb]);
-          ptx::umma_commit(&S.wempty[qw % NW]);
+          UCOMMIT_E(&S.p2_rdx[pb]);
+          UCOMMIT_E(&S.wempty[qw % NW]);
           if (j > 0) issue_dW(j - 1);
         }
         issue_dW(T - 1);
-        ptx::umma_commit(&S.p0_ok);   // D', delta and the X ring are free for the next field's pass 0
+        UCOMMIT_E(&S.p0_ok);   // D', delta and the X ring are free for the next field's pass 0
       }
     }
     __syncwarp();

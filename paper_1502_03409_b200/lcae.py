@@ -11,7 +11,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblcae.so")
+LIB_PATH = os.environ.get("LCAE_LIB") or os.path.join(_HERE, "liblcae.so")  # LCAE_LIB: A/B another build
 
 LCAE_OK, LCAE_ERR_CONFIG, LCAE_ERR_DATA, LCAE_ERR_NUMERIC, LCAE_ERR_CUDA, LCAE_ERR_ARG = 0, 2, 3, 4, 5, 7
 FP32, BF16 = 0, 1
