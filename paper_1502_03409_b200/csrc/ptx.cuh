@@ -116,6 +116,10 @@ __device__ __forceinline__ void st_u4_ef(void *p, uint4 v, uint64_t pol) {
                "r"(v.w), "l"(pol));
 }
 
+__device__ __forceinline__ void st_u2_ef(void *p, uint2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(v.x), "r"(v.y), "l"(pol));
+}
+
 // Plain (non-tensor) bulk copy global -> shared completing on an mbarrier (bytes multiple of 16).
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(

@@ -105,8 +105,8 @@ lcae_status tc_alloc(lcae_layer *L) {
   LCAE_CK(cudaMalloc(&s->da_part, (size_t)g.F * s->CB * 4));
   LCAE_CK(cudaMalloc(&s->db_part, (size_t)g.F * s->CB * g.n * 4));
   LCAE_CK(cudaMalloc(&s->rowsq_part, (size_t)g.F * s->CB * 2 * tc::KP * 4));
-  LCAE_CK(cudaMalloc(&s->trace, 32 * sizeof(unsigned long long)));
-  LCAE_CK(cudaMemset(s->trace, 0, 32 * sizeof(unsigned long long)));
+  LCAE_CK(cudaMalloc(&s->trace, 48 * sizeof(unsigned long long)));
+  LCAE_CK(cudaMemset(s->trace, 0, 48 * sizeof(unsigned long long)));
   // Wb is [F][KP][n_al] (pad rows zero) for the bf16 path
   cudaFree(L->Wb);
   LCAE_CK(cudaMalloc(&L->Wb, (size_t)g.F * tc::KP * L->n_al * 2));
@@ -170,6 +170,7 @@ lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled) {
   P.n_al = L->n_al;
   P.wp = L->wp;
   P.mode = update ? 1 : 0;
+  P.dbg = getenv("LCAE_DEBUG_FLAGS") ? atoi(getenv("LCAE_DEBUG_FLAGS")) : 0;
   P.want_pooled = want_pooled ? 1 : 0;
   P.keep_grads = L->cfg.keep_grads;
   P.lam = L->cfg.lambda_;
@@ -238,8 +239,8 @@ extern "C" lcae_status lcae_dev_trace(lcae_layer *L, int enable, unsigned long l
   if (!L || !L->tc) { set_error("lcae_dev_trace: bf16 layer required"); return LCAE_ERR_ARG; }
   if (out32) {
     LCAE_CK(cudaStreamSynchronize(L->st));
-    LCAE_CK(cudaMemcpy(out32, L->tc->trace, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    LCAE_CK(cudaMemset(L->tc->trace, 0, 32 * sizeof(unsigned long long)));
+    LCAE_CK(cudaMemcpy(out32, L->tc->trace, 48 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    LCAE_CK(cudaMemset(L->tc->trace, 0, 48 * sizeof(unsigned long long)));
   }
   L->tc->trace_on = enable ? 1 : 0;
   return LCAE_OK;

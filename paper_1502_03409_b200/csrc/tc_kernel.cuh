@@ -55,6 +55,8 @@ struct Params {
   const uint32_t *xpieces;  // [T][XPMAX]: off (16 b) | dst row (8 b) << 16 | log2 rows (8 b) << 24; 0xFFFFFFFF ends
   Geo g;
   int T, mp, CB, n_al, wp, mode, want_pooled, keep_grads;
+  int dbg;   // dev-only (LCAE_DEBUG_FLAGS): bit 0 skips the dX reductions, bit 1 the W~/shadow stores,
+             // bit 2 all epilogue arithmetic (hand-offs kept; for pipeline-ceiling measurements only)
   float lam, eps, lr, mu;
   const __nv_bfloat16 *xt;
   float *dxt;
@@ -90,7 +92,7 @@ struct __align__(1024) Smem {
   uint64_t p2_rdx[2], p2_dw[2], p2_empty[2];
   uint64_t recv_full, peer_free;
   uint32_t tmem_base;
-  unsigned long long tr[32];   // optional wait-cycle trace (lcae_dev_trace)
+  unsigned long long tr[48];   // optional wait-cycle / section trace (lcae_dev_trace)
 };
 
 #define UMMA_E(...) do { if (ptx::elect_one()) ptx::umma_bf16(__VA_ARGS__); __syncwarp(); } while (0)
@@ -157,7 +159,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
   } while (0)
 
   // ---- one-time setup
-  if (threadIdx.x < 32) S.tr[threadIdx.x] = 0ull;
+  if (threadIdx.x < 48) S.tr[threadIdx.x] = 0ull;
+  long long tmark = 0;
+#define TMARK(IDX)                                                                               \
+  do {                                                                                           \
+    if (trec) {                                                                                  \
+      const long long t_ = clock64();                                                            \
+      if ((IDX) >= 0) atomicAdd(&S.tr[(IDX) < 0 ? 0 : (IDX)], (unsigned long long)(t_ - tmark)); \
+      tmark = t_;                                                                                \
+    }                                                                                            \
+  } while (0)
   for (int t = threadIdx.x; t < T * NT; t += NTHREADS) {
     int ry = t / g.RW, rem = t - ry * g.RW;
     S.off[t] = (uint16_t)(t < n ? ry * g.W * g.C + rem : 0);
@@ -441,7 +452,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       const float a = P.alpha[f];
       const float *bf_ = S.bs;
       double jr = 0.0, js = 0.0;
-      float dap = 0.f, rsq = 0.f;
+      float dap = 0.f, rsq4[4] = {0.f, 0.f, 0.f, 0.f};   // rsq4[i]: row 8i + lane/4 of this warp
+      TMARK(-1);
       // ------------------------------------------------ E0: pooling / sparsity, H' (filters [64 half, +64))
       TWAIT(11, ptx::mbar_wait(&S.u_full, nf & 1));
       ptx::tc_fence_after();
@@ -474,6 +486,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&S.h_ready);
+      TMARK(32);
       // ------------------------------------------------ E1: residual, delta, db (pass 1)
 #pragma unroll 1
       for (int j = 0; j < T; ++j, ++ur) {
@@ -519,6 +532,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         }
       }
       if (step) {
+        TMARK(33);
         // ---------------------------------------------- E1b: D = sigma.G~ + lambda h/s, dalpha, D'
         TWAIT(16, ptx::mbar_wait(&S.g_full, nf & 1));
         ptx::tc_fence_after();
@@ -556,10 +570,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&S.d_ready);
+        TMARK(34);
         // ---------------------------------------------- E2: dX, dW, fused projected SGD (pass 2)
-        const float sg_r = S.sig[row];
         const uint64_t pol_ef = ptx::policy_evict_first();   // W~ master / shadow streams
-        const float inv_sg = 1.f / sg_r;
 #pragma unroll 1
         for (int j = 0; j < T; ++j, ++u2) {
           const uint32_t pb = u2 & 1, base = 192 * pb;
@@ -580,6 +593,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             if (lane == 0) ptx::mbar_arrive(&S.dl_full[db_]);
             ++ud;
           }
+          TMARK(35);
           // dx = alpha W^T D - delta, overlap-added into the image gradient with 16-byte reductions:
           // 4x4 lane transposes give each lane 4 consecutive samples of one column.
           {
@@ -604,19 +618,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               t1 = __shfl_xor_sync(0xffffffffu, o2 ? a1 : a3, 2);
               if (o2) { a0 = t0; a1 = t1; } else { a2 = t0; a3 = t1; }
               const int nn = j * NT + hc + 4 * blk + r4;
-              if (nn < n && grp_ok) red_v4(dcol + (int64_t)S.off[nn] * mp, a0, a1, a2, a3);
+              if (nn < n && grp_ok && !(P.dbg & 1)) red_v4(dcol + (int64_t)S.off[nn] * mp, a0, a1, a2, a3);
             }
           }
-          // dW_j (lanes = filter rows, this warp's 32 columns): prefetch the owned W~ run, sum the batch slices
-          // over the cluster, then projected SGD. CTA c owns the 16-column chunk [16c, 16c+16) of each half.
-          constexpr int NC = CB > 1 ? 16 : 32, NV = NC / 4;
+          TMARK(36);
+          // dW_j (lanes = filter rows, this warp's 32 columns). CTA c owns the 16-column chunk [16c, 16c+16) of
+          // each half; the batch slices of that chunk are summed over the cluster (DSMEM), then the projected SGD
+          // runs in a coalesced layout: the summed chunk is transposed through this warp's 2 KB staging slice
+          // (its rows of `recv`) so that lane l updates rows 8i + l/4, columns 4(l%4)..+3 (64-byte row runs).
+          constexpr int NC = CB > 1 ? 16 : 32, NCH = NC / 16;
           const int oc = CB > 1 ? 16 * (int)crank : 0;
-          const int c0 = j * NT + hc + oc;   // multiple of 16: 64-byte aligned in the padded rows
-          float4 wv[NV];
-          float *wr = P.W + ((int64_t)f * k + min(row, k - 1)) * P.wp + c0;
+          const int rr = lane >> 2, cq = lane & 3;
+          const int64_t wrow0 = (int64_t)f * k + qd * 32 + rr;   // W~ master row of i = 0
+          float4 wv[4 * NCH];   // owned W~ runs, coalesced layout (issued before the dW wait)
 #pragma unroll
-          for (int v = 0; v < NV; ++v)
-            wv[v] = (c0 + 4 * v < P.wp) ? ptx::ld_f4_ef(wr + 4 * v, pol_ef) : make_float4(0, 0, 0, 0);
+          for (int h = 0; h < NCH; ++h) {
+            const int cc0 = j * NT + hc + oc + 16 * h + 4 * cq;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int r = qd * 32 + 8 * i + rr;
+              wv[4 * h + i] = (r < k && cc0 < P.wp) ? ptx::ld_f4_ef(P.W + (wrow0 + 8 * i) * P.wp + cc0, pol_ef)
+                                                    : make_float4(0, 0, 0, 0);
+            }
+          }
           TWAIT(21, ptx::mbar_wait(&S.p2_dw[pb], (u2 >> 1) & 1));
           ptx::tc_fence_after();
           float dw[32];
@@ -626,6 +650,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&S.p2_empty[pb]);   // TMEM buffer pb fully read by this warp
+          float *stg = &S.recv[half][qd * 32][0];              // [32 rows][16] fp32, 16-byte chunks swizzled
+          const int swr = (lane >> 1) & 3;                     // swizzle of this lane's row (row = lane)
           if (CB > 1) {
             if (crank) {   // owned chunk to dw[0..15], the peer's chunk to dw[16..31]
 #pragma unroll
@@ -639,73 +665,71 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             const uint32_t rbar = ptx::mapa(ptx::smem_u32(&S.recv_full), peer);
 #pragma unroll
             for (int t = 0; t < 4; ++t)
-              ptx::st_async_v4(rdst + 16 * t, make_float4(dw[16 + 4 * t], dw[17 + 4 * t], dw[18 + 4 * t], dw[19 + 4 * t]),
-                               rbar);
+              ptx::st_async_v4(rdst + 16 * (t ^ swr),
+                               make_float4(dw[16 + 4 * t], dw[17 + 4 * t], dw[18 + 4 * t], dw[19 + 4 * t]), rbar);
             TWAIT(22, ptx::mbar_wait(&S.recv_full, u2 & 1));
+          }
+          float4 dq[4 * NCH];   // summed dW chunk(s), coalesced layout
+#pragma unroll
+          for (int h = 0; h < NCH; ++h) {
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-              const float4 r4 = *reinterpret_cast<const float4 *>(&S.recv[half][row][4 * t]);
-              dw[4 * t] += r4.x;
-              dw[4 * t + 1] += r4.y;
-              dw[4 * t + 2] += r4.z;
-              dw[4 * t + 3] += r4.w;
+              float4 *q = reinterpret_cast<float4 *>(stg + lane * 16 + 4 * (t ^ swr));
+              float4 v = make_float4(dw[16 * h + 4 * t], dw[16 * h + 4 * t + 1], dw[16 * h + 4 * t + 2],
+                                     dw[16 * h + 4 * t + 3]);
+              if (CB > 1) {   // + the peer's batch slice (received in place)
+                const float4 r4 = *q;
+                v.x += r4.x; v.y += r4.y; v.z += r4.z; v.w += r4.w;
+              }
+              *q = v;
             }
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_remote_relaxed(ptx::mapa(ptx::smem_u32(&S.peer_free), peer));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int r = 8 * i + rr;
+              dq[4 * h + i] = *reinterpret_cast<const float4 *>(stg + r * 16 + 4 * (cq ^ ((r >> 1) & 3)));
+            }
+            __syncwarp();
           }
-          if (row < k) {
-            float4 vv[NV];
-            if (P.vW) {
-              const float *vr = P.vW + ((int64_t)f * k + row) * P.wp + c0;
+          if (CB > 1 && lane == 0)   // staging slice read back: the peer may write the next tile
+            ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&S.peer_free), crank ^ 1u));
+          if (!(P.dbg & 2)) {
 #pragma unroll
-              for (int v = 0; v < NV; ++v)
-                vv[v] = (c0 + 4 * v < P.wp) ? *reinterpret_cast<const float4 *>(vr + 4 * v) : make_float4(0, 0, 0, 0);
-            }
-            float wn[NC];
+            for (int h = 0; h < NCH; ++h) {
+              const int cc0 = j * NT + hc + oc + 16 * h + 4 * cq;
 #pragma unroll
-            for (int t = 0; t < NC; ++t) {
-              const float d = (c0 + t < n) ? dw[t] * inv_sg : 0.f;   // accumulator holds sigma_r * dJ/dW
-              dw[t] = d;
-              float upd = -P.lr * d;
-              if (P.vW) {
-                float vo = (&vv[t >> 2].x)[t & 3];
-                upd = fmaf(P.mu, vo, upd);
-                (&vv[t >> 2].x)[t & 3] = upd;
+              for (int i = 0; i < 4; ++i) {
+                const int r = qd * 32 + 8 * i + rr;
+                if (r >= k || cc0 >= P.wp) continue;
+                const float sg = S.sig[r], isg = 1.f / sg;
+                const int64_t wo = (wrow0 + 8 * i) * P.wp + cc0;
+                float4 vv = make_float4(0, 0, 0, 0);
+                if (P.vW) vv = *reinterpret_cast<const float4 *>(P.vW + wo);
+                float d[4] = {dq[4 * h + i].x, dq[4 * h + i].y, dq[4 * h + i].z, dq[4 * h + i].w};
+                float vo[4] = {vv.x, vv.y, vv.z, vv.w};
+                const float wo4[4] = {wv[4 * h + i].x, wv[4 * h + i].y, wv[4 * h + i].z, wv[4 * h + i].w};
+                float wn[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  d[e] = (cc0 + e < n) ? d[e] * isg : 0.f;   // accumulator holds sigma_r * dJ/dW
+                  float upd = -P.lr * d[e];
+                  if (P.vW) { upd = fmaf(P.mu, vo[e], upd); vo[e] = upd; }
+                  wn[e] = fmaf(sg, wo4[e], upd);
+                  rsq4[i] = fmaf(wn[e], wn[e], rsq4[i]);
+                }
+                ptx::st_f4_ef(P.W + wo, make_float4(wn[0], wn[1], wn[2], wn[3]), pol_ef);
+                if (cc0 < P.n_al)
+                  ptx::st_u2_ef(P.Wb + ((int64_t)f * KP + r) * P.n_al + cc0,
+                                make_uint2(ptx::pack_bf16x2(wn[0], wn[1]), ptx::pack_bf16x2(wn[2], wn[3])), pol_ef);
+                if (P.vW) *reinterpret_cast<float4 *>(P.vW + wo) = make_float4(vo[0], vo[1], vo[2], vo[3]);
+                if (P.keep_grads) *reinterpret_cast<float4 *>(P.gW + wo) = make_float4(d[0], d[1], d[2], d[3]);
               }
-              wn[t] = fmaf(sg_r, (&wv[t >> 2].x)[t & 3], upd);
-              rsq = fmaf(wn[t], wn[t], rsq);
-            }
-#pragma unroll
-            for (int v = 0; v < NV; ++v)
-              if (c0 + 4 * v < P.wp)
-                ptx::st_f4_ef(wr + 4 * v, make_float4(wn[4 * v], wn[4 * v + 1], wn[4 * v + 2], wn[4 * v + 3]), pol_ef);
-            __nv_bfloat16 *br = P.Wb + ((int64_t)f * KP + row) * P.n_al + c0;
-#pragma unroll
-            for (int v = 0; v < NC / 8; ++v)
-              if (c0 + 8 * v < P.n_al) {
-                uint4 q4;
-                q4.x = ptx::pack_bf16x2(wn[8 * v], wn[8 * v + 1]);
-                q4.y = ptx::pack_bf16x2(wn[8 * v + 2], wn[8 * v + 3]);
-                q4.z = ptx::pack_bf16x2(wn[8 * v + 4], wn[8 * v + 5]);
-                q4.w = ptx::pack_bf16x2(wn[8 * v + 6], wn[8 * v + 7]);
-                ptx::st_u4_ef(br + 8 * v, q4, pol_ef);
-              }
-            if (P.vW) {
-              float *vr = P.vW + ((int64_t)f * k + row) * P.wp + c0;
-#pragma unroll
-              for (int v = 0; v < NV; ++v)
-                if (c0 + 4 * v < P.wp) *reinterpret_cast<float4 *>(vr + 4 * v) = vv[v];
-            }
-            if (P.keep_grads) {
-              float *gr = P.gW + ((int64_t)f * k + row) * P.wp + c0;
-#pragma unroll
-              for (int v = 0; v < NV; ++v)
-                if (c0 + 4 * v < P.wp)
-                  *reinterpret_cast<float4 *>(gr + 4 * v) = make_float4(dw[4 * v], dw[4 * v + 1], dw[4 * v + 2], dw[4 * v + 3]);
             }
           }
+          TMARK(37);
         }
       }
+      TMARK(step ? 38 : 33);
       // ------------------------------------------------ per-field partial sums (fixed order)
       jr = warp_sum(jr);
       js = warp_sum(js);
@@ -720,7 +744,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         P.loss_part[((int64_t)f * CB + crank) * 2 + 1] = (double)P.lam * a1;
         P.da_part[(int64_t)f * CB + crank] = a2;
       }
-      if (step) P.rowsq_part[(((int64_t)f * CB + crank) * 2 + half) * KP + row] = rsq;
+      if (step) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {   // the 4 lanes of a row run hold its partial sums
+          float v = rsq4[i];
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          if ((lane & 3) == 0) P.rowsq_part[(((int64_t)f * CB + crank) * 2 + half) * KP + qd * 32 + 8 * i + (lane >> 2)] = v;
+        }
+      }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&S.tmem_free);
@@ -731,8 +763,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
                       (unsigned long long)(clock64() - t_start));
   ptx::tc_fence_before();
   __syncthreads();
-  if (P.trace && threadIdx.x < 32) atomicAdd(&P.trace[threadIdx.x], S.tr[threadIdx.x]);
+  if (P.trace && threadIdx.x < 48) atomicAdd(&P.trace[threadIdx.x], S.tr[threadIdx.x]);
 #undef TWAIT
+#undef TMARK
   if (CB > 1) ptx::cluster_sync();
   if (warp == 1) ptx::tmem_dealloc<512>(tb);
 }

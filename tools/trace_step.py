@@ -16,7 +16,8 @@ NAMES = {0: "mma:wfull", 1: "mma:p0full", 2: "mma:tmem_free", 3: "mma:h_ready", 
          10: "mma:TOTAL", 11: "epi:u_full", 12: "epi:r_full", 13: "epi:p1full", 14: "epi:dl_empty(E1)",
          16: "epi:g_full", 18: "epi:p2_rdx", 19: "epi:xfull", 20: "epi:dl_empty(E2)", 21: "epi:p2_dw",
          22: "epi:dsmem", 24: "xprod:TOTAL", 25: "wprod:TOTAL", 26: "epi:TOTAL", 27: "wprod:wempty",
-         28: "xprod:p0_ok", 29: "xprod:p0empty", 30: "xprod:p1", 31: "xprod:xempty"}
+         28: "xprod:p0_ok", 29: "xprod:p0empty", 30: "xprod:p1", 31: "xprod:xempty",
+         32: "sec:E0", 33: "sec:E1 loop", 34: "sec:E1b", 35: "sec:E2a resid+delta", 36: "sec:E2b dX", 37: "sec:E2c dW+SGD", 38: "sec:field end", 39: "sec:E2b0 dX tmem load"}
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
@@ -37,7 +38,7 @@ for _ in range(steps):
     L.step(x, None, want_loss=False)
 torch.cuda.synchronize()
 ms, nl = L.profile_read()
-out = (C.c_ulonglong * 32)()
+out = (C.c_ulonglong * 48)()
 lcae.check(lib.lcae_dev_trace(L.h, 0, out))
 ctas = min(shape.fields * ((shape.batch + 127) // 128), 148 // ((shape.batch + 127) // 128) * ((shape.batch + 127) // 128))
 per = lambda v: v / ctas / steps  # noqa: E731
