@@ -116,6 +116,9 @@ __device__ __forceinline__ void st_u4_ef(void *p, uint4 v, uint64_t pol) {
                "r"(v.w), "l"(pol));
 }
 
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ void st_u2_ef(void *p, uint2 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(v.x), "r"(v.y), "l"(pol));
 }

@@ -81,7 +81,7 @@ struct TcScratch {
   unsigned long long *trace = nullptr;
   size_t smem = 0;
   double *loss_part = nullptr;
-  float *da_part = nullptr, *db_part = nullptr, *rowsq_part = nullptr;
+  float *da_part = nullptr, *db_part = nullptr, *rowsq_part = nullptr, *dbscr = nullptr;
   CUtensorMap tmW;
   CUtensorMap tmX[tc::NXMAP];
   uint32_t *xpieces = nullptr;
@@ -105,6 +105,7 @@ lcae_status tc_alloc(lcae_layer *L) {
   LCAE_CK(cudaMalloc(&s->da_part, (size_t)g.F * s->CB * 4));
   LCAE_CK(cudaMalloc(&s->db_part, (size_t)g.F * s->CB * g.n * 4));
   LCAE_CK(cudaMalloc(&s->rowsq_part, (size_t)g.F * s->CB * 2 * tc::KP * 4));
+  LCAE_CK(cudaMalloc(&s->dbscr, (size_t)s->grid * 4 * tc::MAX_NPAD * 4));   // per-CTA db partials (L2)
   LCAE_CK(cudaMalloc(&s->trace, 48 * sizeof(unsigned long long)));
   LCAE_CK(cudaMemset(s->trace, 0, 48 * sizeof(unsigned long long)));
   // Wb is [F][KP][n_al] (pad rows zero) for the bf16 path
@@ -150,7 +151,7 @@ lcae_status tc_alloc(lcae_layer *L) {
 void tc_free(lcae_layer *L) {
   if (!L->tc) return;
   TcScratch *s = L->tc;
-  for (void *p : {(void *)s->loss_part, (void *)s->da_part, (void *)s->db_part, (void *)s->rowsq_part, (void *)s->trace, (void *)s->xpieces})
+  for (void *p : {(void *)s->loss_part, (void *)s->da_part, (void *)s->db_part, (void *)s->rowsq_part, (void *)s->trace, (void *)s->xpieces, (void *)s->dbscr})
     if (p) cudaFree(p);
   delete s;
   L->tc = nullptr;
@@ -190,6 +191,7 @@ lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled) {
   P.da_part = s->da_part;
   P.db_part = s->db_part;
   P.rowsq_part = s->rowsq_part;
+  P.dbscr = s->dbscr;
   P.gW = L->gW;
   P.trace = s->trace_on ? s->trace : nullptr;
   if (update) LCAE_CK(cudaMemsetAsync(L->dxt, 0, (size_t)g.H * g.W * g.C * L->mp * 4, L->st));

@@ -5,14 +5,14 @@
 // streams bf16 W~_f tiles (TMA, 128B swizzle, 4-stage ring) and its X_f patch rows (cp.async gather from the
 // batch-innermost HWCN image) in three passes over n-tiles of 64:
 //
-//   pass 0  U^T   = X^T W~^T                   (M = samples, N = k, K = n)      TMEM [0,128)
+//   pass 0  U^T   = X^T W~^T                   (M = samples, N = k, K = n)      TMEM [384,512)
 //           E0: u = sigma.U~, h = alpha u, s_G = sqrt(eps + sum_G h^2), J_s, p; H' = bf16(sigma.h) -> smem
-//   pass 1  R^T_j - X_j^T = H'^T W~_j + X_j^T (-I)   (M = samples, N = 64)       TMEM [128,384) (4 buffers)
+//   pass 1  R^T_j - X_j^T = H'^T W~_j + X_j^T (-I)   (M = samples, N = 64)       TMEM [0,256) (4 buffers)
 //           E1: e = (R - x) + b, J_r, delta = 2e -> smem (bf16), db partial (butterfly column sums)
-//           G^T  += delta_j^T W~_j^T  (lag 2)  (M = samples, N = k, K = 64)     TMEM [384,512)
+//           G^T  += delta_j^T W~_j^T  (lag 2)  (M = samples, N = k, K = 64)     TMEM [256,384)
 //           E1b: D = sigma.G~ + lambda h/s, dalpha, D' = bf16(sigma alpha D) -> smem
 //   pass 2  R^T_j - X_j^T (recompute delta), dX^T_j = D'^T W~_j; dx = dX - delta -> red.global.v4 into dX
-//           dW_j = H' delta_j^T + D' X_j^T     (M = k, N = 64, K = 2 x samples) TMEM 2 x [R|dX|dW]
+//           dW_j = H' delta_j^T + D' X_j^T     (M = k, N = 64, K = 2 x samples) TMEM 2 x [R|dX|dW] in [0,384)
 //           E2: sum the batch slices of dW_j over the cluster (DSMEM), projected-SGD of W~ (fp32 master +
 //               bf16 shadow, 16-byte vectors), row sums of squares for the new row scale sigma.
 //
@@ -21,9 +21,11 @@
 // W = sigma (.) W~ with a per-row scale sigma ("lazy projection"): the unit-norm projection of
 // PAPER.md:89 is applied by the finalize kernel as sigma' = 1/||W~'_row||, so the update never re-reads W.
 //
-// Warp roles: 0 = W TMA producer, 1 = MMA issuer (one lane), 2-9 = epilogue (TMEM lane quarter = warp % 4,
-// column half = (warp - 2) / 4), 10 = X cp.async producer. X tiles of pass 0 borrow the D'/delta buffers (idle
-// during pass 0) as a 4-slot ring, those of pass 1 the D' buffer, those of pass 2 a dedicated 2-slot ring.
+// U lives outside the pass-2 columns, so the next field's pass 0 overlaps this field's last pass-2 epilogue tiles.
+// Warp roles: 0 = W TMA producer, 1 = MMA issuer (warp-uniform, elected lane issues), 2-9 = epilogue (TMEM lane
+// quarter = warp % 4, column half = (warp - 2) / 4), 10 = X TMA producer. X tiles of pass 0 borrow the D', delta,
+// pass-2 X and H' buffers (all idle during pass 0) as an 8-slot ring, those of pass 1 the D' buffer, those of
+// pass 2 a dedicated 2-slot ring.
 #pragma once
 #include <algorithm>
 
@@ -36,11 +38,11 @@ namespace tc {
 constexpr int KP = 128;        // filters padded to one TMEM lane block
 constexpr int NT = 64;         // n-tile
 constexpr int MC = 128;        // samples per CTA
-constexpr int NW = 4;          // W ring stages
+constexpr int NW = 3;          // W ring stages
 constexpr int NX = 2;          // pass-2 X ring stages
-constexpr int NP0 = 4;         // pass-0 X ring slots (D'[0..1], delta[0..1])
+constexpr int NP0 = 8;         // pass-0 X ring slots (D'[0..1], delta[0..1], pass-2 X ring [0..1], H'[0..1])
 constexpr int NRB = 4;         // pass-1 R buffers
-constexpr int GLAG = 2;        // G_j issued after R_{j+GLAG}
+constexpr int GLAG = 1;        // G_j issued after R_{j+GLAG}
 constexpr int NEPI = 8;        // epilogue warps
 constexpr int XWARP = 2 + NEPI;
 constexpr int NTHREADS = 32 * (XWARP + 1);
@@ -67,7 +69,8 @@ struct Params {
   double *loss_part;   // [F][CB][2]
   float *da_part;      // [F][CB]
   float *db_part;      // [F][CB][n]
-  float *rowsq_part;   // [F][CB][KP]
+  float *rowsq_part;   // [F][CB][2][KP]
+  float *dbscr;        // [grid][4][MAX_NPAD]: per-lane-quarter db partials of the current field
   float *gW;
   unsigned long long *trace;   // nullable: per-role wait cycles summed over CTAs
 };
@@ -80,14 +83,14 @@ struct __align__(1024) Smem {
   uint8_t Dl[2][16384];      // pass 0: X slots 2,3
   uint8_t negI[8192];        // -I (64 x 64 bf16, SW128)
   float recv[2][128][16];    // peer's dW partial for this CTA's owned 16-column chunks, [half][row][col]
+  float stg[NEPI][32][16];   // per-warp transpose staging of the own dW chunk (16-byte chunks swizzled)
   uint16_t off[MAX_NPAD];    // pixel-feature offset of patch row n inside the field window (host-checked < 2^16)
   float bs[MAX_NPAD];        // b_f of the current field (epilogue)
   float sig[KP];
-  float dbw[2][NEPI][32];
   double redd[NEPI][2];
   float redf[NEPI];
   uint64_t wfull[NW], wempty[NW], xfull[NX], xempty[NX], p0full[NP0], p0empty[NP0], p1full[2], p1empty[2];
-  uint64_t p0_ok, u_full, h_ready, g_full, d_ready, tmem_free;
+  uint64_t p0_ok, u_full, h_ready, g_full, d_ready;
   uint64_t r_full[NRB], r_empty[NRB], dl_full[2], dl_empty[2];
   uint64_t p2_rdx[2], p2_dw[2], p2_empty[2];
   uint64_t recv_full, peer_free;
@@ -98,7 +101,10 @@ struct __align__(1024) Smem {
 #define UMMA_E(...) do { if (ptx::elect_one()) ptx::umma_bf16(__VA_ARGS__); __syncwarp(); } while (0)
 #define UCOMMIT_E(bar) do { if (ptx::elect_one()) ptx::umma_commit(bar); __syncwarp(); } while (0)
 
-__device__ __forceinline__ uint8_t *p0slot(Smem &S, int i) { return i < 2 ? S.D + i * 16384 : S.Dl[i - 2]; }
+// pass 0 borrows every operand buffer the previous field's pass 2 is done with (all free at p0_ok)
+__device__ __forceinline__ uint8_t *p0slot(Smem &S, int i) {
+  return i < 2 ? S.D + i * 16384 : i < 4 ? S.Dl[i - 2] : i < 6 ? S.Xr[i - 4] : S.H + (i - 6) * 16384;
+}
 
 // store 8 consecutive bf16 (cols c0..c0+7 of row `row`) into a [rows][64] SW128 block
 __device__ __forceinline__ void st8(uint8_t *blk, int row, int c0, const float *v) {
@@ -193,7 +199,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     ptx::mbar_init(&S.h_ready, NEPI);
     ptx::mbar_init(&S.g_full, 1);
     ptx::mbar_init(&S.d_ready, NEPI);
-    ptx::mbar_init(&S.tmem_free, NEPI);
     for (int i = 0; i < NRB; ++i) { ptx::mbar_init(&S.r_full[i], 1); ptx::mbar_init(&S.r_empty[i], NEPI); }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&S.dl_full[i], NEPI);
@@ -262,7 +267,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         }
         __syncwarp();
       };
-      // pass 0 ring borrows the D'/delta buffers: wait until the previous field is done with them
+      // pass 0 ring borrows the D'/delta/X/H' buffers: wait until the previous field is done with them
       if (step) TWAIT(28, ptx::mbar_wait(&S.p0_ok, (nf & 1) ^ 1));
       for (int j = 0; j < T; ++j, ++q0) {
         const int s = q0 % NP0;
@@ -322,8 +327,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         }
       };
       for (int f = cid; f < g.F; f += ncl, ++nf) {
-        TWAIT(2, ptx::mbar_wait(&S.tmem_free, (nf & 1) ^ 1));
-        ptx::tc_fence_after();
         // ---- pass 0: U^T = X^T W~^T
         for (int j = 0; j < T; ++j, ++qw, ++q0) {
           wait_w(qw);
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           for (int kk = 0; kk < NT / 16; ++kk) {
             uint64_t ad = ptx::sdesc_sw128(xs + kk * 2048, 8192, 1024);
             uint64_t bd = ptx::sdesc_sw128(wst(qw) + kk * 32, 16, 1024);
-            UMMA_E(tb + 0, ad, bd, id_enc, (j | kk) != 0);
+            UMMA_E(tb + 384, ad, bd, id_enc, (j | kk) != 0);
           }
           UCOMMIT_E(&S.wempty[qw % NW]);
           UCOMMIT_E(&S.p0empty[q0 % NP0]);
@@ -356,7 +359,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           for (int kk = 0; kk < NT / 16; ++kk) {
             uint64_t ad = ptx::sdesc_sw128(dl + kk * 32, 16, 1024);
             uint64_t bd = ptx::sdesc_sw128(wst(qj) + kk * 32, 16, 1024);
-            UMMA_E(tb + 384, ad, bd, id_g, (j | kk) != 0);
+            UMMA_E(tb + 256, ad, bd, id_g, (j | kk) != 0);
           }
           UCOMMIT_E(&S.dl_empty[db_]);
           UCOMMIT_E(&S.wempty[qj % NW]);
@@ -369,8 +372,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           TWAIT(1, ptx::mbar_wait(&S.p1full[s1], (q1 >> 1) & 1));
           ptx::tc_fence_after();
           ptx::fence_proxy_async_smem();
-          mma_aw(128 + 64 * rb, sH, wst(qw));
-          mma_negx(128 + 64 * rb, sD + s1 * 16384);
+          mma_aw(64 * rb, sH, wst(qw));
+          mma_negx(64 * rb, sD + s1 * 16384);
           UCOMMIT_E(&S.r_full[rb]);
           UCOMMIT_E(&S.p1empty[s1]);
           if (step) {
@@ -460,8 +463,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
 #pragma unroll 1
       for (int cc = 2 * half; cc < 2 * half + 2; ++cc) {
         float u[32];
-        ptx::tmem_ld16(tl + cc * 32, u);
-        ptx::tmem_ld16(tl + cc * 32 + 16, u + 16);
+        ptx::tmem_ld16(tl + 384 + cc * 32, u);
+        ptx::tmem_ld16(tl + 384 + cc * 32 + 16, u + 16);
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int t = 0; t < 32; ++t) u[t] *= S.sig[cc * 32 + t];
@@ -494,8 +497,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         TWAIT(12, ptx::mbar_wait(&S.r_full[rb], (ur / NRB) & 1));
         ptx::tc_fence_after();
         float rv[32];
-        ptx::tmem_ld16(tl + 128 + 64 * rb + hc, rv);
-        ptx::tmem_ld16(tl + 128 + 64 * rb + hc + 16, rv + 16);
+        ptx::tmem_ld16(tl + 64 * rb + hc, rv);
+        ptx::tmem_ld16(tl + 64 * rb + hc + 16, rv + 16);
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         __syncwarp();
@@ -521,14 +524,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               rv[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
             }
           }
-          S.dbw[j & 1][ew][lane] = rv[0];
-          ptx::named_bar_sync(1, 32 * NEPI);
-          if ((ew & 3) == 0) {
-            const int nn = j * NT + hc + lane;
-            const float sdb = S.dbw[j & 1][ew][lane] + S.dbw[j & 1][ew + 1][lane] + S.dbw[j & 1][ew + 2][lane] +
-                              S.dbw[j & 1][ew + 3][lane];
-            if (nn < n) P.db_part[((int64_t)f * CB + crank) * n + nn] = sdb;
-          }
+          // this lane quarter's partial; the four quarters are summed once per field (no per-tile barrier)
+          P.dbscr[((size_t)blockIdx.x * 4 + qd) * MAX_NPAD + j * NT + hc + lane] = rv[0];
         }
       }
       if (step) {
@@ -539,10 +536,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
 #pragma unroll 1
         for (int cc = 2 * half; cc < 2 * half + 2; ++cc) {
           float u[32], gg[32];
-          ptx::tmem_ld16(tl + cc * 32, u);
-          ptx::tmem_ld16(tl + cc * 32 + 16, u + 16);
-          ptx::tmem_ld16(tl + 384 + cc * 32, gg);
-          ptx::tmem_ld16(tl + 384 + cc * 32 + 16, gg + 16);
+          ptx::tmem_ld16(tl + 384 + cc * 32, u);
+          ptx::tmem_ld16(tl + 384 + cc * 32 + 16, u + 16);
+          ptx::tmem_ld16(tl + 256 + cc * 32, gg);
+          ptx::tmem_ld16(tl + 256 + cc * 32 + 16, gg + 16);
           ptx::tmem_ld_wait();
 #pragma unroll
           for (int t = 0; t < 32; ++t) u[t] *= S.sig[cc * 32 + t];
@@ -573,6 +570,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         TMARK(34);
         // ---------------------------------------------- E2: dX, dW, fused projected SGD (pass 2)
         const uint64_t pol_ef = ptx::policy_evict_first();   // W~ master / shadow streams
+        constexpr int NC = CB > 1 ? 16 : 32, NCH = NC / 16;
+        const int oc = CB > 1 ? 16 * (int)crank : 0;
+        const int rr = lane >> 2, cq = lane & 3;
+        const int64_t wrow0 = (int64_t)f * k + qd * 32 + rr;   // W~ master row of i = 0
 #pragma unroll 1
         for (int j = 0; j < T; ++j, ++u2) {
           const uint32_t pb = u2 & 1, base = 192 * pb;
@@ -626,10 +627,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           // each half; the batch slices of that chunk are summed over the cluster (DSMEM), then the projected SGD
           // runs in a coalesced layout: the summed chunk is transposed through this warp's 2 KB staging slice
           // (its rows of `recv`) so that lane l updates rows 8i + l/4, columns 4(l%4)..+3 (64-byte row runs).
-          constexpr int NC = CB > 1 ? 16 : 32, NCH = NC / 16;
-          const int oc = CB > 1 ? 16 * (int)crank : 0;
-          const int rr = lane >> 2, cq = lane & 3;
-          const int64_t wrow0 = (int64_t)f * k + qd * 32 + rr;   // W~ master row of i = 0
           float4 wv[4 * NCH];   // owned W~ runs, coalesced layout (issued before the dW wait)
 #pragma unroll
           for (int h = 0; h < NCH; ++h) {
@@ -650,7 +647,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&S.p2_empty[pb]);   // TMEM buffer pb fully read by this warp
-          float *stg = &S.recv[half][qd * 32][0];              // [32 rows][16] fp32, 16-byte chunks swizzled
+          TMARK(40);
+          float *stg = &S.stg[ew][0][0];                       // [32 rows][16] fp32, 16-byte chunks swizzled
+          const float *rcv = &S.recv[half][qd * 32][0];        // same layout, written by the peer
           const int swr = (lane >> 1) & 3;                     // swizzle of this lane's row (row = lane)
           if (CB > 1) {
             if (crank) {   // owned chunk to dw[0..15], the peer's chunk to dw[16..31]
@@ -667,32 +666,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             for (int t = 0; t < 4; ++t)
               ptx::st_async_v4(rdst + 16 * (t ^ swr),
                                make_float4(dw[16 + 4 * t], dw[17 + 4 * t], dw[18 + 4 * t], dw[19 + 4 * t]), rbar);
-            TWAIT(22, ptx::mbar_wait(&S.recv_full, u2 & 1));
           }
+          TMARK(41);
           float4 dq[4 * NCH];   // summed dW chunk(s), coalesced layout
 #pragma unroll
           for (int h = 0; h < NCH; ++h) {
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              float4 *q = reinterpret_cast<float4 *>(stg + lane * 16 + 4 * (t ^ swr));
-              float4 v = make_float4(dw[16 * h + 4 * t], dw[16 * h + 4 * t + 1], dw[16 * h + 4 * t + 2],
-                                     dw[16 * h + 4 * t + 3]);
-              if (CB > 1) {   // + the peer's batch slice (received in place)
-                const float4 r4 = *q;
-                v.x += r4.x; v.y += r4.y; v.z += r4.z; v.w += r4.w;
-              }
-              *q = v;
-            }
+            for (int t = 0; t < 4; ++t)
+              *reinterpret_cast<float4 *>(stg + lane * 16 + 4 * (t ^ swr)) =
+                  make_float4(dw[16 * h + 4 * t], dw[16 * h + 4 * t + 1], dw[16 * h + 4 * t + 2], dw[16 * h + 4 * t + 3]);
             __syncwarp();
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const int r = 8 * i + rr;
-              dq[4 * h + i] = *reinterpret_cast<const float4 *>(stg + r * 16 + 4 * (cq ^ ((r >> 1) & 3)));
+              const int r = 8 * i + rr, o = r * 16 + 4 * (cq ^ ((r >> 1) & 3));
+              dq[4 * h + i] = *reinterpret_cast<const float4 *>(stg + o);
             }
             __syncwarp();
           }
-          if (CB > 1 && lane == 0)   // staging slice read back: the peer may write the next tile
-            ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&S.peer_free), crank ^ 1u));
+          if (CB > 1) {   // + the peer's batch slice, read straight from the receive slice in the same layout
+            TWAIT(22, ptx::mbar_wait(&S.recv_full, u2 & 1));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int r = 8 * i + rr, o = r * 16 + 4 * (cq ^ ((r >> 1) & 3));
+              const float4 r4 = *reinterpret_cast<const float4 *>(rcv + o);
+              dq[i].x += r4.x; dq[i].y += r4.y; dq[i].z += r4.z; dq[i].w += r4.w;
+            }
+            __syncwarp();
+            if (lane == 0)   // receive slice read: the peer may send the next tile (reads only; relaxed suffices)
+              ptx::mbar_arrive_remote_relaxed(ptx::mapa(ptx::smem_u32(&S.peer_free), crank ^ 1u));
+          }
+          TMARK(42);
           if (!(P.dbg & 2)) {
 #pragma unroll
             for (int h = 0; h < NCH; ++h) {
@@ -736,6 +739,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       dap = warp_sum(dap);
       if (lane == 0) { S.redd[ew][0] = jr; S.redd[ew][1] = js; S.redf[ew] = dap; }
       ptx::named_bar_sync(1, 32 * NEPI);
+      if (step) {   // db of this CTA's samples: the four lane quarters' partials (fixed order)
+        const float *d = P.dbscr + (size_t)blockIdx.x * 4 * MAX_NPAD;
+        for (int t = etid; t < n; t += 32 * NEPI)
+          P.db_part[((int64_t)f * CB + crank) * n + t] = ((d[t] + d[MAX_NPAD + t]) + d[2 * MAX_NPAD + t]) + d[3 * MAX_NPAD + t];
+      }
       if (etid == 0) {
         double a0 = 0.0, a1 = 0.0;
         float a2 = 0.f;
@@ -755,7 +763,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&S.tmem_free);
     }
   }
   // ---- teardown
