@@ -252,13 +252,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       // X_j = runs of consecutive image rows (one per receptive-field row): a few TMA boxes per 64-sample half;
       // the 128B swizzle follows the absolute smem address, so boxes may land at any row of the tile.
       auto load_tile = [&](uint8_t *dst_tile, uint64_t *bar, int j) {
-        if (lane == 0) {
-          const int rows = min(NT, n - j * NT);
-          ptx::mbar_arrive_expect_tx(bar, (uint32_t)rows * 128u * 2u);
-          const uint32_t *pc = P.xpieces + j * XPMAX;
-          for (int p = 0; p < XPMAX; ++p) {
-            const uint32_t w = __ldg(pc + p);
-            if (w == 0xFFFFFFFFu) break;
+        // the whole warp reads the tile's piece table at once (one load latency, not one per piece) and every
+        // lane issues the TMA boxes of its own pieces
+        static_assert(XPMAX == 64, "two piece words per lane");
+        const uint32_t *pc = P.xpieces + j * XPMAX;
+        const uint32_t w0 = __ldg(pc + lane), w1 = __ldg(pc + 32 + lane);
+        if (lane == 0) ptx::mbar_arrive_expect_tx(bar, (uint32_t)min(NT, n - j * NT) * 128u * 2u);
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint32_t w = e ? w1 : w0;
+          if (w != 0xFFFFFFFFu) {
             const int offp = (int)(w & 0xFFFFu), dr = (int)((w >> 16) & 0xFFu), lg = (int)(w >> 24);
 #pragma unroll
             for (int h = 0; h < 2; ++h)
