@@ -87,6 +87,7 @@ struct __align__(1024) Smem {
   uint16_t off[MAX_NPAD];    // pixel-feature offset of patch row n inside the field window (host-checked < 2^16)
   float bs[MAX_NPAD];        // b_f of the current field (epilogue)
   float sig[KP];
+  float isig[KP];            // 1 / sig
   double redd[NEPI][2];
   float redf[NEPI];
   uint64_t wfull[NW], wempty[NW], xfull[NX], xempty[NX], p0full[NP0], p0empty[NP0], p1full[2], p1empty[2];
@@ -100,6 +101,8 @@ struct __align__(1024) Smem {
 
 #define UMMA_E(...) do { if (ptx::elect_one()) ptx::umma_bf16(__VA_ARGS__); __syncwarp(); } while (0)
 #define UCOMMIT_E(bar) do { if (ptx::elect_one()) ptx::umma_commit(bar); __syncwarp(); } while (0)
+
+static_assert(offsetof(Smem, bs) % 16 == 0, "float4 reads of b_f");
 
 // pass 0 borrows every operand buffer the previous field's pass 2 is done with (all free at p0_ok)
 __device__ __forceinline__ uint8_t *p0slot(Smem &S, int i) {
@@ -123,11 +126,25 @@ __device__ __forceinline__ void red_v4(float *p, float a, float b, float c, floa
 // e = (R - x) + b over this warp's 32 columns of a tile for this thread's sample; rv <- delta = 2e (masked).
 __device__ __forceinline__ float residual32(float (&rv)[32], int c0, int n, const float *bf_, bool svalid) {
   float jr = 0.f;
+  const float4 *b4 = reinterpret_cast<const float4 *>(bf_ + c0);   // c0 % 32 == 0: 16-byte aligned broadcasts
+  if (svalid && c0 + 32 <= n) {   // full run (all but the ragged last tile): no masking
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 bv = b4[q];
+      const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float e = rv[4 * q + t] + bb[t];
+        jr = fmaf(e, e, jr);
+        rv[4 * q + t] = 2.f * e;
+      }
+    }
+    return jr;
+  }
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
     const int nn = c0 + c;
-    const float bv = nn < n ? bf_[nn] : 0.f;   // smem copy of b_f
-    float e = rv[c] + bv;
+    float e = rv[c] + bf_[nn];   // entries of bs past n are never initialised: selected away below
     e = (svalid && nn < n) ? e : 0.f;
     jr = fmaf(e, e, jr);
     rv[c] = 2.f * e;
@@ -373,7 +390,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           wait_w(qw);
           const uint32_t rb = ur % NRB, s1 = q1 & 1;
           TWAIT(4, ptx::mbar_wait(&S.r_empty[rb], ((ur / NRB) & 1) ^ 1));
-          TWAIT(1, ptx::mbar_wait(&S.p1full[s1], (q1 >> 1) & 1));
+          TWAIT(44, ptx::mbar_wait(&S.p1full[s1], (q1 >> 1) & 1));
           ptx::tc_fence_after();
           ptx::fence_proxy_async_smem();
           mma_aw(64 * rb, sH, wst(qw));
@@ -453,7 +470,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       const int fr = f / g.gc, fc = f - fr * g.gc;
       const int64_t pixbase = ((int64_t)fr * g.s * g.W + (int64_t)fc * g.s) * g.C;
       ptx::named_bar_sync(1, 32 * NEPI);
-      if (etid < KP) S.sig[etid] = etid < k ? P.sigma[(int64_t)f * k + etid] : 1.f;
+      if (etid < KP) {
+        const float sg = etid < k ? P.sigma[(int64_t)f * k + etid] : 1.f;
+        S.sig[etid] = sg;
+        S.isig[etid] = 1.f / sg;
+      }
       for (int t = etid; t < n; t += 32 * NEPI) S.bs[t] = P.b[(int64_t)f * n + t];
       ptx::named_bar_sync(1, 32 * NEPI);
       const float a = P.alpha[f];
@@ -498,7 +519,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
 #pragma unroll 1
       for (int j = 0; j < T; ++j, ++ur) {
         const uint32_t rb = ur % NRB;
-        TWAIT(12, ptx::mbar_wait(&S.r_full[rb], (ur / NRB) & 1));
+        if (j == 0) TWAIT(43, ptx::mbar_wait(&S.r_full[rb], (ur / NRB) & 1));
+        else TWAIT(12, ptx::mbar_wait(&S.r_full[rb], (ur / NRB) & 1));
         ptx::tc_fence_after();
         float rv[32];
         ptx::tmem_ld16(tl + 64 * rb + hc, rv);
@@ -552,8 +574,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             float ss = 0.f;
 #pragma unroll
             for (int t = 0; t < GP; ++t) { float h = a * u[G0 + t]; ss = fmaf(h, h, ss); }
-            const float sG = sqrtf(P.eps + ss);
-            const float inv = sG > 0.f ? P.lam / sG : 0.f;
+            const float v = P.eps + ss;
+            const float inv = v > 0.f ? P.lam * rsqrtf(v) : 0.f;   // lambda / s_G
 #pragma unroll
             for (int t = 0; t < GP; ++t) {
               const int col = cc * 32 + G0 + t;
@@ -708,7 +730,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               for (int i = 0; i < 4; ++i) {
                 const int r = qd * 32 + 8 * i + rr;
                 if (r >= k || cc0 >= P.wp) continue;
-                const float sg = S.sig[r], isg = 1.f / sg;
+                const float sg = S.sig[r], isg = S.isig[r];
                 const int64_t wo = (wrow0 + 8 * i) * P.wp + cc0;
                 float4 vv = make_float4(0, 0, 0, 0);
                 if (P.vW) vv = *reinterpret_cast<const float4 *>(P.vW + wo);
