@@ -82,6 +82,7 @@ struct TcScratch {
   size_t smem = 0;
   double *loss_part = nullptr;
   float *da_part = nullptr, *db_part = nullptr, *rowsq_part = nullptr, *dbscr = nullptr;
+  uint8_t *dscr = nullptr;
   CUtensorMap tmW;
   CUtensorMap tmX[tc::NXMAP];
   uint32_t *xpieces = nullptr;
@@ -106,6 +107,7 @@ lcae_status tc_alloc(lcae_layer *L) {
   LCAE_CK(cudaMalloc(&s->db_part, (size_t)g.F * s->CB * g.n * 4));
   LCAE_CK(cudaMalloc(&s->rowsq_part, (size_t)g.F * s->CB * 2 * tc::KP * 4));
   LCAE_CK(cudaMalloc(&s->dbscr, (size_t)s->grid * 4 * tc::MAX_NPAD * 4));   // per-CTA db partials (L2)
+  LCAE_CK(cudaMalloc(&s->dscr, (size_t)s->grid * T * 16384));   // per-CTA pass-1 delta tiles (L2-resident)
   LCAE_CK(cudaMalloc(&s->trace, 48 * sizeof(unsigned long long)));
   LCAE_CK(cudaMemset(s->trace, 0, 48 * sizeof(unsigned long long)));
   // Wb is [F][KP][n_al] (pad rows zero) for the bf16 path
@@ -151,7 +153,7 @@ lcae_status tc_alloc(lcae_layer *L) {
 void tc_free(lcae_layer *L) {
   if (!L->tc) return;
   TcScratch *s = L->tc;
-  for (void *p : {(void *)s->loss_part, (void *)s->da_part, (void *)s->db_part, (void *)s->rowsq_part, (void *)s->trace, (void *)s->xpieces, (void *)s->dbscr})
+  for (void *p : {(void *)s->loss_part, (void *)s->da_part, (void *)s->db_part, (void *)s->rowsq_part, (void *)s->trace, (void *)s->xpieces, (void *)s->dbscr, (void *)s->dscr})
     if (p) cudaFree(p);
   delete s;
   L->tc = nullptr;
@@ -192,6 +194,7 @@ lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled) {
   P.db_part = s->db_part;
   P.rowsq_part = s->rowsq_part;
   P.dbscr = s->dbscr;
+  P.dscr = s->dscr;
   P.gW = L->gW;
   P.trace = s->trace_on ? s->trace : nullptr;
   if (update) LCAE_CK(cudaMemsetAsync(L->dxt, 0, (size_t)g.H * g.W * g.C * L->mp * 4, L->st));

@@ -8,11 +8,12 @@
 //   pass 0  U^T   = X^T W~^T                   (M = samples, N = k, K = n)      TMEM [384,512)
 //           E0: u = sigma.U~, h = alpha u, s_G = sqrt(eps + sum_G h^2), J_s, p; H' = bf16(sigma.h) -> smem
 //   pass 1  R^T_j - X_j^T = H'^T W~_j + X_j^T (-I)   (M = samples, N = 64)       TMEM [0,256) (4 buffers)
-//           E1: e = (R - x) + b, J_r, delta = 2e -> smem (bf16), db partial (butterfly column sums)
-//           G^T  += delta_j^T W~_j^T  (lag 2)  (M = samples, N = k, K = 64)     TMEM [256,384)
+//           E1: e = (R - x) + b, J_r, delta = 2e -> smem (bf16) and its image to a per-CTA global scratch,
+//               db partial (butterfly column sums)
+//           G^T  += delta_j^T W~_j^T  (lag 1)  (M = samples, N = k, K = 64)     TMEM [256,384)
 //           E1b: D = sigma.G~ + lambda h/s, dalpha, D' = bf16(sigma alpha D) -> smem
-//   pass 2  R^T_j - X_j^T (recompute delta), dX^T_j = D'^T W~_j; dx = dX - delta -> red.global.v4 into dX
-//           dW_j = H' delta_j^T + D' X_j^T     (M = k, N = 64, K = 2 x samples) TMEM 2 x [R|dX|dW] in [0,384)
+//   pass 2  delta_j reloaded (bulk copy, L2), dx^T_j = D'^T W~_j + delta_j^T (-I) -> red.global.v4 into dX
+//           dW_j = H' delta_j^T + D' X_j^T     (M = k, N = 64, K = 2 x samples) TMEM 3 x [dX|dW] in [0,384)
 //           E2: sum the batch slices of dW_j over the cluster (DSMEM), projected-SGD of W~ (fp32 master +
 //               bf16 shadow, 16-byte vectors), row sums of squares for the new row scale sigma.
 //
@@ -42,6 +43,7 @@ constexpr int NW = 3;          // W ring stages
 constexpr int NX = 2;          // pass-2 X ring stages
 constexpr int NP0 = 8;         // pass-0 X ring slots (D'[0..1], delta[0..1], pass-2 X ring [0..1], H'[0..1])
 constexpr int NRB = 4;         // pass-1 R buffers
+constexpr int NB2 = 3;         // pass-2 TMEM buffers [dX | dW] (128 columns each)
 constexpr int GLAG = 1;        // G_j issued after R_{j+GLAG}
 constexpr int NEPI = 8;        // epilogue warps
 constexpr int XWARP = 2 + NEPI;
@@ -71,6 +73,7 @@ struct Params {
   float *db_part;      // [F][CB][n]
   float *rowsq_part;   // [F][CB][2][KP]
   float *dbscr;        // [grid][4][MAX_NPAD]: per-lane-quarter db partials of the current field
+  uint8_t *dscr;       // [grid][T][16 KB]: pass-1 delta tiles (their swizzled smem image), reloaded in pass 2
   float *gW;
   unsigned long long *trace;   // nullable: per-role wait cycles summed over CTAs
 };
@@ -91,9 +94,9 @@ struct __align__(1024) Smem {
   double redd[NEPI][2];
   float redf[NEPI];
   uint64_t wfull[NW], wempty[NW], xfull[NX], xempty[NX], p0full[NP0], p0empty[NP0], p1full[2], p1empty[2];
-  uint64_t p0_ok, u_full, h_ready, g_full, d_ready;
+  uint64_t p0_ok, u_full, h_ready, g_full, d_ready, d_stored;
   uint64_t r_full[NRB], r_empty[NRB], dl_full[2], dl_empty[2];
-  uint64_t p2_rdx[2], p2_dw[2], p2_empty[2];
+  uint64_t p2_full[NB2], p2_empty[NB2], d2full[2], d2empty[2];
   uint64_t recv_full, peer_free;
   uint32_t tmem_base;
   unsigned long long tr[48];   // optional wait-cycle / section trace (lcae_dev_trace)
@@ -120,7 +123,9 @@ __device__ __forceinline__ void st8(uint8_t *blk, int row, int c0, const float *
 }
 
 __device__ __forceinline__ void red_v4(float *p, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+  // no "memory" clobber: the reductions need no ordering against the kernel's other memory operations, and a
+  // clobber would pin every following shared-memory load behind them
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d));
 }
 
 // e = (R - x) + b over this warp's 32 columns of a tile for this thread's sample; rv <- delta = 2e (masked).
@@ -212,17 +217,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     for (int i = 0; i < NP0; ++i) { ptx::mbar_init(&S.p0full[i], 1); ptx::mbar_init(&S.p0empty[i], 1); }
     for (int i = 0; i < 2; ++i) { ptx::mbar_init(&S.p1full[i], 1); ptx::mbar_init(&S.p1empty[i], 1); }
     ptx::mbar_init(&S.p0_ok, 1);
+    for (int i = 0; i < NB2; ++i) { ptx::mbar_init(&S.p2_full[i], 1); ptx::mbar_init(&S.p2_empty[i], NEPI); }
     ptx::mbar_init(&S.u_full, 1);
     ptx::mbar_init(&S.h_ready, NEPI);
     ptx::mbar_init(&S.g_full, 1);
     ptx::mbar_init(&S.d_ready, NEPI);
+    ptx::mbar_init(&S.d_stored, 1);
     for (int i = 0; i < NRB; ++i) { ptx::mbar_init(&S.r_full[i], 1); ptx::mbar_init(&S.r_empty[i], NEPI); }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&S.dl_full[i], NEPI);
-      ptx::mbar_init(&S.dl_empty[i], 1);
-      ptx::mbar_init(&S.p2_rdx[i], 1);
-      ptx::mbar_init(&S.p2_dw[i], 1);
-      ptx::mbar_init(&S.p2_empty[i], NEPI);
+      ptx::mbar_init(&S.dl_empty[i], 2);   // G MMA commit + delta store-out (warp 0 lane 1)
+      ptx::mbar_init(&S.d2full[i], 1);
+      ptx::mbar_init(&S.d2empty[i], 1);
     }
     ptx::mbar_init(&S.recv_full, 1);   // armed per tile with expect_tx; completed by the peer's st.async bytes
     ptx::mbar_init(&S.peer_free, NEPI);
@@ -254,11 +260,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             else
               ptx::tma_load_2d(S.Wr[s], &P.tmW, &S.wfull[s], j * NT, f * KP);
           }
+    } else if (lane == 1 && step) {
+      // =================================================================== delta store-out (bulk S2G)
+      // every pass-1 delta tile goes to this CTA's global scratch as its swizzled smem image; pass 2 reloads it
+      uint32_t ud = 0, nf = 0;
+      for (int f = cid; f < g.F; f += ncl, ++nf) {
+        uint8_t *dst = P.dscr + (size_t)blockIdx.x * T * 16384;
+        for (int j = 0; j < T; ++j, ++ud) {
+          const uint32_t db_ = ud & 1;
+          ptx::mbar_wait(&S.dl_full[db_], (ud >> 1) & 1);
+          ptx::bulk_s2g(dst + (size_t)j * 16384, S.Dl[db_], 16384);
+          ptx::bulk_commit();
+          ptx::bulk_wait_read0();   // smem read done: the epilogue may refill the slot
+          ptx::mbar_arrive(&S.dl_empty[db_]);
+        }
+        ptx::bulk_wait0();                 // all of the field's delta images written
+        ptx::fence_proxy_async_global();
+        ptx::mbar_arrive(&S.d_stored);
+      }
     }
     __syncwarp();
   } else if (warp == XWARP) {
     // =================================================================== X producer (cp.async gather)
-    uint32_t q0 = 0, q1 = 0, qx = 0, nf = 0;
+    uint32_t q0 = 0, q1 = 0, qx = 0, nf = 0, qd2 = 0;
     if (lane == 0) {
 #pragma unroll
       for (int i = 0; i < NXMAP; ++i) ptx::tma_prefetch(&P.tmX[i]);
@@ -307,7 +331,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           ptx::mbar_wait(&S.p1empty[qq & 1], (qq >> 1) & 1);
         continue;
       }
-      for (int j = 0; j < T; ++j, ++qx) {
+      // pass 2: delta_j (the pass-1 images, once all are stored and the G MMAs are done with the ring) and X_j
+      TWAIT(28, ptx::mbar_wait(&S.d_stored, nf & 1));
+      TWAIT(28, ptx::mbar_wait(&S.g_full, nf & 1));
+      ptx::fence_proxy_async_global();
+      const uint8_t *dsrc = P.dscr + (size_t)blockIdx.x * T * 16384;
+      for (int j = 0; j < T; ++j, ++qx, ++qd2) {
+        const int sd = qd2 & 1;
+        TWAIT(31, ptx::mbar_wait(&S.d2empty[sd], ((qd2 >> 1) & 1) ^ 1));
+        if (lane == 0) {
+          ptx::mbar_arrive_expect_tx(&S.d2full[sd], 16384);
+          ptx::bulk_g2s(S.Dl[sd], dsrc + (size_t)j * 16384, 16384, &S.d2full[sd]);
+        }
+        __syncwarp();
         const int s = qx % NX;
         TWAIT(31, ptx::mbar_wait(&S.xempty[s], ((qx / NX) & 1) ^ 1));
         load_tile(S.Xr[s], &S.xfull[s], j);
@@ -322,8 +358,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       const uint32_t id_g = ptx::idesc_bf16(128, KP, false, false);
       const uint32_t id_dw1 = ptx::idesc_bf16(128, NT, true, true);
       const uint32_t id_dw2 = ptx::idesc_bf16(128, NT, true, false);
+      const uint32_t id_nd = ptx::idesc_bf16(128, NT, false, false);   // delta^T (-I)
       const uint32_t sH = ptx::smem_u32(S.H), sD = ptx::smem_u32(S.D), sNI = ptx::smem_u32(S.negI);
-      uint32_t qw = 0, q0 = 0, q1 = 0, qx = 0, nf = 0, ur = 0, ud = 0, u2 = 0;
+      uint32_t qw = 0, q0 = 0, q1 = 0, qx = 0, nf = 0, ur = 0, ud = 0, u2 = 0, qd2 = 0;
       auto wst = [&](uint32_t qq) { return ptx::smem_u32(S.Wr[qq % NW]); };
       auto wait_w = [&](uint32_t qq) {
         TWAIT(0, ptx::mbar_wait(&S.wfull[qq % NW], (qq / NW) & 1));
@@ -406,49 +443,47 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         if (!step) continue;
         for (int j = std::max(0, T - GLAG); j < T; ++j) issue_G(j);
         UCOMMIT_E(&S.g_full);
-        // ---- pass 2: R_j - X_j and dX_j (W stage released), then dW_j one tile behind
+        // ---- pass 2 (TMEM: NB2 buffers [dX | dW] in [0,384)): delta_j is the pass-1 tile reloaded from global
+        //   dx^T_j = D'^T W~_j + delta_j^T (-I)   (alpha folded into D')
+        //   dW_j   = H' delta_j^T + D' X_j^T
         TWAIT(6, ptx::mbar_wait(&S.d_ready, nf & 1));
         ptx::tc_fence_after();
         ptx::fence_proxy_async_smem();
-        const uint32_t u2_0 = u2, qx0 = qx;
-        auto issue_dW = [&](int j) {
-          const uint32_t pb = (u2_0 + j) & 1, db_ = ud & 1, xsl = (qx0 + j) % NX;
-          TWAIT(8, ptx::mbar_wait(&S.dl_full[db_], (ud >> 1) & 1));
+        for (int j = 0; j < T; ++j, ++qw, ++u2, ++qx, ++qd2) {
+          const uint32_t pb = u2 % NB2, xsl = qx % NX, sd = qd2 & 1;
+          const uint32_t dcol = 128 * pb;
+          wait_w(qw);
+          TWAIT(8, ptx::mbar_wait(&S.d2full[sd], (qd2 >> 1) & 1));
+          TWAIT(7, ptx::mbar_wait(&S.p2_empty[pb], ((u2 / NB2) & 1) ^ 1));
           ptx::tc_fence_after();
-          ptx::fence_proxy_async_smem();
-          const uint32_t dl = ptx::smem_u32(S.Dl[db_]), dcol = 192 * pb + 128, xs = ptx::smem_u32(S.Xr[xsl]);
+          mma_aw(dcol, sD, wst(qw));   // D'^T W~_j
+          const uint32_t dl = ptx::smem_u32(S.Dl[sd]);
+#pragma unroll
+          for (int kk = 0; kk < NT / 16; ++kk) {   // + delta_j^T (-I)
+            uint64_t ad = ptx::sdesc_sw128(dl + kk * 32, 16, 1024);
+            uint64_t bd = ptx::sdesc_sw128(sNI + kk * 32, 16, 1024);
+            UMMA_E(tb + dcol, ad, bd, id_nd, 1);
+          }
+          UCOMMIT_E(&S.wempty[qw % NW]);
 #pragma unroll
           for (int kk = 0; kk < MC / 16; ++kk) {   // H' delta_j^T  (K = samples)
             uint64_t ad = ptx::sdesc_sw128(sH + kk * 2048, 16384, 1024);
             uint64_t bd = ptx::sdesc_sw128(dl + kk * 2048, 16384, 1024);
-            UMMA_E(tb + dcol, ad, bd, id_dw1, kk > 0);
+            UMMA_E(tb + dcol + 64, ad, bd, id_dw1, kk > 0);
           }
+          TWAIT(9, ptx::mbar_wait(&S.xfull[xsl], (qx / NX) & 1));
+          ptx::tc_fence_after();
+          const uint32_t xs = ptx::smem_u32(S.Xr[xsl]);
 #pragma unroll
           for (int kk = 0; kk < MC / 16; ++kk) {   // + D' X_j^T
             uint64_t ad = ptx::sdesc_sw128(sD + kk * 2048, 16384, 1024);
             uint64_t bd = ptx::sdesc_sw128(xs + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
-            UMMA_E(tb + dcol, ad, bd, id_dw2, 1);
+            UMMA_E(tb + dcol + 64, ad, bd, id_dw2, 1);
           }
-          UCOMMIT_E(&S.p2_dw[pb]);
-          UCOMMIT_E(&S.dl_empty[db_]);
+          UCOMMIT_E(&S.p2_full[pb]);
+          UCOMMIT_E(&S.d2empty[sd]);
           UCOMMIT_E(&S.xempty[xsl]);
-          ++ud;
-        };
-        for (int j = 0; j < T; ++j, ++qw, ++u2, ++qx) {
-          wait_w(qw);
-          const uint32_t pb = u2 & 1, xsl = qx % NX;
-          TWAIT(9, ptx::mbar_wait(&S.xfull[xsl], (qx / NX) & 1));
-          TWAIT(7, ptx::mbar_wait(&S.p2_empty[pb], ((u2 >> 1) & 1) ^ 1));
-          ptx::tc_fence_after();
-          ptx::fence_proxy_async_smem();
-          mma_aw(192 * pb, sH, wst(qw));                    // R^T_j
-          mma_negx(192 * pb, ptx::smem_u32(S.Xr[xsl]));     //   - X_j^T
-          mma_aw(192 * pb + 64, sD, wst(qw));               // dX^T_j (alpha folded into D')
-          UCOMMIT_E(&S.p2_rdx[pb]);
-          UCOMMIT_E(&S.wempty[qw % NW]);
-          if (j > 0) issue_dW(j - 1);
         }
-        issue_dW(T - 1);
         UCOMMIT_E(&S.p0_ok);   // D', delta and the X ring are free for the next field's pass 0
       }
     }
@@ -534,6 +569,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           const uint32_t db_ = ud & 1;
           TWAIT(14, ptx::mbar_wait(&S.dl_empty[db_], ((ud >> 1) & 1) ^ 1));
 #pragma unroll
+#pragma unroll
           for (int c = 0; c < 32; c += 8) st8(S.Dl[db_], row, hc + c, rv + c);
           ptx::fence_proxy_async_smem();
           __syncwarp();
@@ -602,42 +638,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         const int64_t wrow0 = (int64_t)f * k + qd * 32 + rr;   // W~ master row of i = 0
 #pragma unroll 1
         for (int j = 0; j < T; ++j, ++u2) {
-          const uint32_t pb = u2 & 1, base = 192 * pb;
-          TWAIT(18, ptx::mbar_wait(&S.p2_rdx[pb], (u2 >> 1) & 1));
+          const uint32_t pb = u2 % NB2, base = 128 * pb;
+          TWAIT(18, ptx::mbar_wait(&S.p2_full[pb], (u2 / NB2) & 1));
           ptx::tc_fence_after();
-          float rv[32];
-          ptx::tmem_ld16(tl + base + hc, rv);
-          ptx::tmem_ld16(tl + base + hc + 16, rv + 16);
-          ptx::tmem_ld_wait();
-          residual32(rv, j * NT + hc, n, bf_, svalid);
-          {
-            const uint32_t db_ = ud & 1;
-            TWAIT(20, ptx::mbar_wait(&S.dl_empty[db_], ((ud >> 1) & 1) ^ 1));
-#pragma unroll
-            for (int c = 0; c < 32; c += 8) st8(S.Dl[db_], row, hc + c, rv + c);
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&S.dl_full[db_]);
-            ++ud;
-          }
           TMARK(35);
-          // dx = alpha W^T D - delta, overlap-added into the image gradient with 16-byte reductions:
-          // 4x4 lane transposes give each lane 4 consecutive samples of one column.
+          // dx = alpha W^T D - delta (both halves accumulated in TMEM), overlap-added into the image gradient with
+          // 16-byte reductions: 4x4 lane transposes give each lane 4 consecutive samples of one column.
           {
             const int r4 = lane & 3;
             const bool o1 = r4 & 1, o2 = r4 & 2;
             float *dcol = P.dxt + pixbase * mp + (s0 + qd * 32 + (lane & ~3));
             const bool grp_ok = s0 + qd * 32 + (lane & ~3) < mp;
+            float t8[8];
 #pragma unroll
             for (int blk = 0; blk < 8; ++blk) {
               if ((blk & 1) == 0) {   // TMEM loads in 8-column pieces keep the register footprint small
-                float t8[8];
-                ptx::tmem_ld8(tl + base + 64 + hc + 4 * blk, t8);
+                ptx::tmem_ld8(tl + base + hc + 4 * blk, t8);
                 ptx::tmem_ld_wait();
-#pragma unroll
-                for (int q = 0; q < 8; ++q) rv[4 * blk + q] = t8[q] - rv[4 * blk + q];   // rv <- dx
               }
-              float a0 = rv[4 * blk], a1 = rv[4 * blk + 1], a2 = rv[4 * blk + 2], a3 = rv[4 * blk + 3];
+              const int q = 4 * (blk & 1);
+              float a0 = t8[q], a1 = t8[q + 1], a2 = t8[q + 2], a3 = t8[q + 3];
               float t0 = __shfl_xor_sync(0xffffffffu, o1 ? a0 : a1, 1);
               float t1 = __shfl_xor_sync(0xffffffffu, o1 ? a2 : a3, 1);
               if (o1) { a0 = t0; a2 = t1; } else { a1 = t0; a3 = t1; }
@@ -664,11 +684,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
                                                     : make_float4(0, 0, 0, 0);
             }
           }
-          TWAIT(21, ptx::mbar_wait(&S.p2_dw[pb], (u2 >> 1) & 1));
-          ptx::tc_fence_after();
           float dw[32];
-          ptx::tmem_ld16(tl + base + 128 + hc, dw);
-          ptx::tmem_ld16(tl + base + 128 + hc + 16, dw + 16);
+          ptx::tmem_ld16(tl + base + 64 + hc, dw);
+          ptx::tmem_ld16(tl + base + 64 + hc + 16, dw + 16);
           ptx::tmem_ld_wait();
           ptx::tc_fence_before();
           __syncwarp();
