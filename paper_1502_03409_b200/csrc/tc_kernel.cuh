@@ -649,15 +649,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             const bool o1 = r4 & 1, o2 = r4 & 2;
             float *dcol = P.dxt + pixbase * mp + (s0 + qd * 32 + (lane & ~3));
             const bool grp_ok = s0 + qd * 32 + (lane & ~3) < mp;
-            float t8[8];
+            float xv[32];
+            ptx::tmem_ld16(tl + base + hc, xv);
+            ptx::tmem_ld16(tl + base + hc + 16, xv + 16);
+            ptx::tmem_ld_wait();
 #pragma unroll
             for (int blk = 0; blk < 8; ++blk) {
-              if ((blk & 1) == 0) {   // TMEM loads in 8-column pieces keep the register footprint small
-                ptx::tmem_ld8(tl + base + hc + 4 * blk, t8);
-                ptx::tmem_ld_wait();
-              }
-              const int q = 4 * (blk & 1);
-              float a0 = t8[q], a1 = t8[q + 1], a2 = t8[q + 2], a3 = t8[q + 3];
+              float a0 = xv[4 * blk], a1 = xv[4 * blk + 1], a2 = xv[4 * blk + 2], a3 = xv[4 * blk + 3];
               float t0 = __shfl_xor_sync(0xffffffffu, o1 ? a0 : a1, 1);
               float t1 = __shfl_xor_sync(0xffffffffu, o1 ? a2 : a3, 1);
               if (o1) { a0 = t0; a2 = t1; } else { a1 = t0; a3 = t1; }
