@@ -193,3 +193,41 @@ extern "C" lcae_status lcae_dev_tma_offset_selftest(const void *src, int rows, i
   LCAE_CK(cudaDeviceSynchronize());
   return LCAE_OK;
 }
+
+// ---- dev hook: the thread <- (lane, column) map of tcgen05.ld.16x256b.x2 (out: [4 warps][2 halves][32][8])
+namespace lcae {
+__global__ void __launch_bounds__(128) tmem_shape_kernel(uint32_t *out) {
+  __shared__ uint32_t tbase_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) ptx::tmem_alloc<32>(&tbase_s);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tb = tbase_s, tl = tb + ((uint32_t)(warp * 32) << 16);
+  uint32_t r[16];
+  for (int c = 0; c < 16; ++c) r[c] = ((uint32_t)(warp * 32 + lane) << 8) | (uint32_t)c;
+  ptx::tmem_st16(tl, r);
+  ptx::tmem_st_wait();
+  __syncwarp();
+  for (int h = 0; h < 2; ++h) {
+    float v[8];
+    ptx::tmem_ld_16x256b_x2(tl + ((uint32_t)(16 * h) << 16), v);
+    ptx::tmem_ld_wait();
+    for (int i = 0; i < 8; ++i) out[((warp * 2 + h) * 32 + lane) * 8 + i] = __float_as_uint(v[i]);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) ptx::tmem_dealloc<32>(tb);
+}
+}  // namespace lcae
+
+extern "C" lcae_status lcae_dev_tmem_shape_selftest(uint32_t *host_out) {
+  uint32_t *d = nullptr;
+  LCAE_CK(cudaMalloc(&d, 4 * 2 * 32 * 8 * 4));
+  tmem_shape_kernel<<<1, 128>>>(d);
+  LCAE_CK(cudaGetLastError());
+  LCAE_CK(cudaMemcpy(host_out, d, 4 * 2 * 32 * 8 * 4, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  return LCAE_OK;
+}
+

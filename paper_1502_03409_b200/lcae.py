@@ -65,6 +65,7 @@ def _load():
         "lcae_dev_umma_selftest": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P]),
         "lcae_dev_tma_selftest": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P]),
         "lcae_dev_red_probe": (C.c_int, [P, C.c_int64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
+        "lcae_dev_tmem_shape_selftest": (C.c_int, [P]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

@@ -73,3 +73,22 @@ def test_red_probe_reports(torch_cuda, capsys):
         out[mode] = elems / (ms.value * 1e-3) / 1e9
     with capsys.disabled():
         print(f"\n[red probe] G elem/s: red.f32={out[0]:.1f} red.v4.f32={out[1]:.1f} ld+add+st={out[2]:.1f}")
+
+
+@pytest.mark.gpu
+def test_tmem_16x256b_thread_map():
+    """tcgen05.ld.16x256b.x2: thread t holds rows t/4 and t/4 + 8 of the 16-lane block, columns 2(t%4), +1 of
+    each 8-column half (the map ptx.cuh documents)."""
+    from paper_1502_03409_b200 import lcae
+    out = np.zeros((4, 2, 32, 8), dtype=np.uint32)
+    lcae.lib.lcae_dev_tmem_shape_selftest.argtypes = [C.c_void_p]
+    lcae.check(lcae.lib.lcae_dev_tmem_shape_selftest(out.ctypes.data))
+    for w in range(4):
+        for h in range(2):
+            for t in range(32):
+                got = [(int(v) >> 8, int(v) & 255) for v in out[w, h, t]]
+                r0 = 32 * w + 16 * h + t // 4
+                c = 2 * (t % 4)
+                want = [(r0, c), (r0, c + 1), (r0 + 8, c), (r0 + 8, c + 1),
+                        (r0, c + 8), (r0, c + 9), (r0 + 8, c + 8), (r0 + 8, c + 9)]
+                assert got == want, (w, h, t, got, want)
