@@ -102,17 +102,26 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+_X64 = {}
+
+
 def cpu_oracle_rate(shape, budget_s=12.0, seed=0):
     """Time the fp64 oracle (as it stands) on a bounded field sample; return images/s extrapolated to the
-    whole layer (every field costs the same work) plus a description."""
+    whole layer (every field costs the same work) plus a description. The sample grows geometrically but never
+    past the time budget's estimate, so one call takes about budget_s."""
     from oracle import lcae_oracle as O
     geo = dict(img_h=shape.img_h, img_w=shape.img_w, img_c=shape.img_c, rf_h=shape.rf_h, rf_w=shape.rf_w,
                stride=shape.stride, pool_group=shape.pool_group, lam=shape.lam, eps=shape.eps)
-    X = make_images(shape, seed=1).astype(np.float64)
+    if shape.name not in _X64:
+        _X64[shape.name] = make_images(shape, seed=1).astype(np.float64)
+    X = _X64[shape.name]
     done, t_used = 0, 0.0
     order = stratified_fields(shape, shape.fields, seed=seed)
     while t_used < budget_s and done < shape.fields:
-        nb = min(max(1, done or 4), shape.fields - done)
+        nb = max(1, done or 4)
+        if done:   # stay within the budget: at most the fields the remaining time affords
+            nb = min(nb, max(1, int((budget_s - t_used) / (t_used / done))))
+        nb = min(nb, shape.fields - done)
         fl = order[done:done + nb]
         W, a, b = make_params(shape, seed=0, fields=fl)
         t0 = time.perf_counter()
@@ -132,10 +141,12 @@ def run_reference(args, shape):
     if rank != 0:
         return
     steps = []
+    # each step is a bounded sample of the workload; the whole --steps/--warmup run stays near 150 s
+    per = min(args.ref_budget, max(1.0, 150.0 / (args.steps + args.warmup / 4)))
     for _ in range(args.warmup):
-        cpu_oracle_rate(shape, budget_s=args.ref_budget / 4)
+        cpu_oracle_rate(shape, budget_s=per / 4)
     for _ in range(args.steps):
-        v, done, t_used, threads = cpu_oracle_rate(shape, budget_s=args.ref_budget)
+        v, done, t_used, threads = cpu_oracle_rate(shape, budget_s=per)
         steps.append((v, done, t_used))
     v = statistics.median(s[0] for s in steps)
     sample = (f"{steps[0][1]} of {shape.fields} fields per step (stratified), extrapolated linearly; "
