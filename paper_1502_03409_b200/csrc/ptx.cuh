@@ -141,6 +141,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// Predicated 16-byte reduction (no branch around it); no "memory" clobber, as for red_v4.
+__device__ __forceinline__ void red_v4_if(float *p, float a, float b, float c, float d, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t@p red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
+      "f"(a), "f"(b), "f"(c), "f"(d), "r"((int)pred));
+}
 // Bulk copy shared -> global (bulk-group completion; bytes multiple of 16).
 __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)

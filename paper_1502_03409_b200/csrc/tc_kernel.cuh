@@ -535,7 +535,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           for (int t = 0; t < GP; ++t) { float h = a * u[G0 + t]; ss = fmaf(h, h, ss); }
           const int G = (cc * 32 + G0) / GP;
           if (G < ng && svalid) {
-            float sG = sqrtf(P.eps + ss);
+            const float v = P.eps + ss;
+            const float sG = v > 0.f ? v * rsqrtf(v) : 0.f;   // sqrt(eps + sum_G h^2)
             js += (double)sG;
             if (P.want_pooled) P.pooled[(((int64_t)gi * g.gr + fr) * g.gc + fc) * ng + G] = sG;
           }
@@ -636,6 +637,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         const int oc = CB > 1 ? 16 * (int)crank : 0;
         const int rr = lane >> 2, cq = lane & 3;
         const int64_t wrow0 = (int64_t)f * k + qd * 32 + rr;   // W~ master row of i = 0
+        // per-field invariants of this thread's E2 work, hoisted out of the tile loop
+        const bool do_red = !(P.dbg & 1), do_sgd = !(P.dbg & 2), has_v = P.vW != nullptr, keep = P.keep_grads != 0;
+        float *const dxcol = P.dxt + pixbase * mp + (s0 + qd * 32 + (lane & ~3));   // dX band of this lane group
+        const bool grp_ok = s0 + qd * 32 + (lane & ~3) < mp;
+        const float *wrp[4];
+        float sgr[4], isgr[4];
+        bool rok[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = qd * 32 + 8 * i + rr;
+          rok[i] = r < k;
+          wrp[i] = P.W + (wrow0 + 8 * i) * P.wp + hc + oc + 4 * cq;
+          sgr[i] = S.sig[r];
+          isgr[i] = S.isig[r];
+        }
 #pragma unroll 1
         for (int j = 0; j < T; ++j, ++u2) {
           const uint32_t pb = u2 % NB2, base = 128 * pb;
@@ -647,8 +663,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           {
             const int r4 = lane & 3;
             const bool o1 = r4 & 1, o2 = r4 & 2;
-            float *dcol = P.dxt + pixbase * mp + (s0 + qd * 32 + (lane & ~3));
-            const bool grp_ok = s0 + qd * 32 + (lane & ~3) < mp;
+            const bool full = (j + 1) * NT <= n;   // all but the ragged last tile
             float xv[32];
             ptx::tmem_ld16(tl + base + hc, xv);
             ptx::tmem_ld16(tl + base + hc + 16, xv + 16);
@@ -663,7 +678,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               t1 = __shfl_xor_sync(0xffffffffu, o2 ? a1 : a3, 2);
               if (o2) { a0 = t0; a1 = t1; } else { a2 = t0; a3 = t1; }
               const int nn = j * NT + hc + 4 * blk + r4;
-              if (nn < n && grp_ok && !(P.dbg & 1)) red_v4(dcol + (int64_t)S.off[nn] * mp, a0, a1, a2, a3);
+              ptx::red_v4_if(dxcol + (uint32_t)S.off[nn] * (uint32_t)mp, a0, a1, a2, a3,
+                        (full || nn < n) && grp_ok && do_red);
             }
           }
           TMARK(36);
@@ -676,15 +692,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           for (int h = 0; h < NCH; ++h) {
             const int cc0 = j * NT + hc + oc + 16 * h + 4 * cq;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int r = qd * 32 + 8 * i + rr;
-              wv[4 * h + i] = (r < k && cc0 < P.wp) ? ptx::ld_f4_ef(P.W + (wrow0 + 8 * i) * P.wp + cc0, pol_ef)
-                                                    : make_float4(0, 0, 0, 0);
-            }
+            for (int i = 0; i < 4; ++i)
+              wv[4 * h + i] = (rok[i] && cc0 < P.wp) ? ptx::ld_f4_ef(wrp[i] + j * NT + 16 * h, pol_ef)
+                                                     : make_float4(0, 0, 0, 0);
           }
-          float dw[32];
-          ptx::tmem_ld16(tl + base + 64 + hc, dw);
-          ptx::tmem_ld16(tl + base + 64 + hc + 16, dw + 16);
+          float dw[32];   // CB = 2: dw[0..15] = the owned chunk, dw[16..31] = the peer's chunk
+          ptx::tmem_ld16(tl + base + 64 + hc + (CB > 1 ? 16 * crank : 0), dw);
+          ptx::tmem_ld16(tl + base + 64 + hc + (CB > 1 ? 16 * (1 - crank) : 16), dw + 16);
           ptx::tmem_ld_wait();
           ptx::tc_fence_before();
           __syncwarp();
@@ -694,10 +708,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           const float *rcv = &S.recv[half][qd * 32][0];        // same layout, written by the peer
           const int swr = (lane >> 1) & 3;                     // swizzle of this lane's row (row = lane)
           if (CB > 1) {
-            if (crank) {   // owned chunk to dw[0..15], the peer's chunk to dw[16..31]
-#pragma unroll
-              for (int t = 0; t < 16; ++t) { float tmp = dw[t]; dw[t] = dw[t + 16]; dw[t + 16] = tmp; }
-            }
             const uint32_t peer = crank ^ 1u;
             // arm this tile's receive phase: 8 warps x 32 rows x 16 floats arrive from the peer via st.async
             if (etid == 0) ptx::mbar_arrive_expect_tx(&S.recv_full, 2 * 128 * 16 * 4);
@@ -738,36 +748,38 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               ptx::mbar_arrive_remote_relaxed(ptx::mapa(ptx::smem_u32(&S.peer_free), crank ^ 1u));
           }
           TMARK(42);
-          if (!(P.dbg & 2)) {
+          if (do_sgd) {
+            const bool fullc = (j + 1) * NT <= n;   // no column of this tile past n
+            const float nlr = -P.lr;
 #pragma unroll
             for (int h = 0; h < NCH; ++h) {
               const int cc0 = j * NT + hc + oc + 16 * h + 4 * cq;
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
+                if (!rok[i] || cc0 >= P.wp) continue;
                 const int r = qd * 32 + 8 * i + rr;
-                if (r >= k || cc0 >= P.wp) continue;
-                const float sg = S.sig[r], isg = S.isig[r];
-                const int64_t wo = (wrow0 + 8 * i) * P.wp + cc0;
-                float4 vv = make_float4(0, 0, 0, 0);
-                if (P.vW) vv = *reinterpret_cast<const float4 *>(P.vW + wo);
-                float d[4] = {dq[4 * h + i].x, dq[4 * h + i].y, dq[4 * h + i].z, dq[4 * h + i].w};
-                float vo[4] = {vv.x, vv.y, vv.z, vv.w};
+                float *wp_ = const_cast<float *>(wrp[i]) + j * NT + 16 * h;   // = W~ + row * wp + cc0
+                const float d0[4] = {dq[4 * h + i].x, dq[4 * h + i].y, dq[4 * h + i].z, dq[4 * h + i].w};
                 const float wo4[4] = {wv[4 * h + i].x, wv[4 * h + i].y, wv[4 * h + i].z, wv[4 * h + i].w};
-                float wn[4];
+                float d[4], wn[4], vo[4] = {0.f, 0.f, 0.f, 0.f};
+                if (has_v) {
+                  const float4 vv = *reinterpret_cast<const float4 *>(P.vW + (wp_ - P.W));
+                  vo[0] = vv.x; vo[1] = vv.y; vo[2] = vv.z; vo[3] = vv.w;
+                }
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                  d[e] = (cc0 + e < n) ? d[e] * isg : 0.f;   // accumulator holds sigma_r * dJ/dW
-                  float upd = -P.lr * d[e];
-                  if (P.vW) { upd = fmaf(P.mu, vo[e], upd); vo[e] = upd; }
-                  wn[e] = fmaf(sg, wo4[e], upd);
+                  d[e] = (fullc || cc0 + e < n) ? d0[e] * isgr[i] : 0.f;   // accumulator holds sigma_r * dJ/dW
+                  float upd = nlr * d[e];
+                  if (has_v) { upd = fmaf(P.mu, vo[e], upd); vo[e] = upd; }
+                  wn[e] = fmaf(sgr[i], wo4[e], upd);
                   rsq4[i] = fmaf(wn[e], wn[e], rsq4[i]);
                 }
-                ptx::st_f4_ef(P.W + wo, make_float4(wn[0], wn[1], wn[2], wn[3]), pol_ef);
+                ptx::st_f4_ef(wp_, make_float4(wn[0], wn[1], wn[2], wn[3]), pol_ef);
                 if (cc0 < P.n_al)
                   ptx::st_u2_ef(P.Wb + ((int64_t)f * KP + r) * P.n_al + cc0,
                                 make_uint2(ptx::pack_bf16x2(wn[0], wn[1]), ptx::pack_bf16x2(wn[2], wn[3])), pol_ef);
-                if (P.vW) *reinterpret_cast<float4 *>(P.vW + wo) = make_float4(vo[0], vo[1], vo[2], vo[3]);
-                if (P.keep_grads) *reinterpret_cast<float4 *>(P.gW + wo) = make_float4(d[0], d[1], d[2], d[3]);
+                if (has_v) *reinterpret_cast<float4 *>(P.vW + (wp_ - P.W)) = make_float4(vo[0], vo[1], vo[2], vo[3]);
+                if (keep) *reinterpret_cast<float4 *>(P.gW + (wp_ - P.W)) = make_float4(d[0], d[1], d[2], d[3]);
               }
             }
           }

@@ -68,6 +68,8 @@ def _load():
         "lcae_dev_tmem_shape_selftest": (C.c_int, [P]),
     }
     for name, (res, args) in sigs.items():
+        if name.startswith("lcae_dev_") and not hasattr(lib, name):
+            continue   # dev hooks are optional (A/B of older builds via LCAE_LIB)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
