@@ -43,6 +43,14 @@ def peaks():
         return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
 
 
+def alg_bytes(shape):
+    """SURVEY.md §8(d) algorithmic bytes per step: fp32 W master read + write (and the velocity's with
+    momentum), alpha / b read + write, the bf16 input and the fp32 dX output."""
+    w = shape.fields * shape.filters * shape.n
+    x = shape.batch * shape.img_h * shape.img_w * shape.img_c
+    return 8.0 * w * (2 if shape.momentum > 0 else 1) + 8.0 * shape.fields * (shape.n + 1) + 2.0 * x + 4.0 * x
+
+
 def model_flops(shape):
     """12 k n m F: encode, decode, backprop-to-code, two weight-gradient products, input gradient."""
     return 12.0 * shape.filters * shape.n * shape.batch * shape.fields
@@ -153,7 +161,7 @@ def run_reference(args, shape):
               f"fp64 numpy oracle, {steps[0][2]:.1f} s per sample")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "images/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * shape.batch / v,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": shape.name, "image": [shape.img_h, shape.img_w, shape.img_c],
                        "rf": shape.rf_h, "stride": shape.stride, "filters": shape.filters,
                        "pool_group": shape.pool_group, "batch": shape.batch, "fields": shape.fields},
@@ -240,10 +248,13 @@ def run_ours(args, shape):
     kern_avg = kern_ms / max(1, kern_n)
     per_kernel_flops = flops / world
     achieved = per_kernel_flops / (kern_avg * 1e-3) / 1e12
+    achieved_gbs = alg_bytes(shape) / world / (kern_avg * 1e-3) / 1e9
+    hbm_bound = alg_bytes(shape) / (pk["hbm"] * 1e9) > flops / (pk["bf16_sus"] * 1e12)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            traffic = json.load(fh).get(shape.name, {}).get("dram_bytes_per_launch")
+            key = shape.name if shape.momentum == 0 else f"{shape.name}_mom{shape.momentum:g}"
+            traffic = json.load(fh).get(key, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
     line = {
@@ -253,13 +264,20 @@ def run_ours(args, shape):
         "config": {"workload": shape.name, "image": [shape.img_h, shape.img_w, shape.img_c], "rf": shape.rf_h,
                    "stride": shape.stride, "filters": shape.filters, "pool_group": shape.pool_group,
                    "batch": shape.batch, "fields": shape.fields, "params": shape.fields * shape.filters * shape.n,
+                   "momentum": shape.momentum,
                    "parallelism": f"mp{world}" if world > 1 else "single",
                    "l2": "working set > L2 (fp32 W master 4 B/param streamed every step)"},
         "tflops": flops / (ms_step * 1e-3) / 1e12,
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
-                     "frac": achieved / pk["bf16_sus"], "traffic": traffic,
-                     "kernel": "lcae::tc::step_kernel", "kernel_ms": kern_avg,
-                     "peak_source": f"{pk['src']} bf16_tflops_sustained (kernel timed inside a long step)"},
+        "roofline": ({"bound": "hbm", "achieved": achieved_gbs, "peak": pk["hbm"], "unit": "GB/s",
+                      "frac": achieved_gbs / pk["hbm"], "traffic": traffic,
+                      "kernel": "lcae::tc::step_kernel", "kernel_ms": kern_avg,
+                      "peak_source": f"{pk['src']} hbm_gbs", "tensor_frac": achieved / pk["bf16_sus"]}
+                     if hbm_bound else
+                     {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
+                      "frac": achieved / pk["bf16_sus"], "traffic": traffic,
+                      "kernel": "lcae::tc::step_kernel", "kernel_ms": kern_avg,
+                      "peak_source": f"{pk['src']} bf16_tflops_sustained (kernel timed inside a long step)",
+                      "hbm_frac": achieved_gbs / pk["hbm"]}),
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "e2e": e2e,
@@ -281,9 +299,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of oracle work per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--momentum", type=float, default=0.0, help="SGD momentum (SURVEY.md §8(f) item 3: 0.9)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     shape = CONFIGS[args.config]
+    if args.momentum:
+        shape = shape.replace(momentum=args.momentum)
     if args.impl == "reference":
         run_reference(args, shape)
     else:
