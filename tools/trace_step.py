@@ -17,7 +17,7 @@ NAMES = {0: "mma:wfull", 1: "mma:p0full", 2: "mma:tmem_free", 3: "mma:h_ready", 
          16: "epi:g_full", 18: "epi:p2_rdx", 19: "epi:xfull", 20: "epi:dl_empty(E2)", 21: "epi:p2_dw",
          22: "epi:dsmem", 24: "xprod:TOTAL", 25: "wprod:TOTAL", 26: "epi:TOTAL", 27: "wprod:wempty",
          28: "xprod:p0_ok", 29: "xprod:p0empty", 30: "xprod:p1", 31: "xprod:xempty",
-         32: "sec:E0", 33: "sec:E1 loop", 34: "sec:E1b", 35: "sec:E2a resid+delta", 36: "sec:E2b dX", 37: "sec:E2c3 SGD+stores", 38: "sec:field end", 39: "sec:E2b0 dX tmem load", 40: "sec:E2c0 dW wait+ld", 41: "sec:E2c1 exchange", 42: "sec:E2c2 staging", 43: "epi:r_full(j=0)", 44: "mma:p1full"}
+         32: "sec:E0", 33: "sec:E1 loop", 34: "sec:E1b", 35: "sec:E2a resid+delta", 36: "sec:E2b dX", 37: "sec:E2c3 SGD+stores", 38: "sec:field end", 39: "sec:E2b0 dX tmem load", 40: "sec:E2c0 dW wait+ld", 41: "sec:E2c1 exchange", 42: "sec:E2c2 staging", 43: "epi:r_full(j=0)", 44: "mma:p1full", 45: "epi:db_full"}
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
