@@ -170,6 +170,107 @@ def run_reference(args, shape):
     print(json.dumps(line), flush=True)
 
 
+INFER_METRIC = "images/sec forward_dataset (encode + L2 pooling + streaming top-5 stimuli)"
+
+
+def run_infer(args, shape):
+    """the inference path (lcae_encode + lcae_topk_update) on the same layer. Images
+    shard across ranks with no exchange (each rank streams its own batches): weak scaling."""
+    import torch
+    from paper_1502_03409_b200 import lcae
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.Stream()
+    pk = peaks()
+    K = 5
+    with torch.cuda.stream(stream):
+        L = lcae.Layer(lcae.make_config(shape, precision=lcae.BF16, stream=stream.cuda_stream))
+        W, a, b = make_params(shape, seed=0)
+        L.set_params(W, a, b)
+        del W
+        units = L.grid_r * L.grid_c * (shape.filters // shape.pool_group)
+        pool = [torch.from_numpy(make_images(shape, seed=1 + rank, index=i)).cuda() for i in range(4)]
+        pooled = torch.empty((shape.batch, units), dtype=torch.float32, device="cuda")
+        vals = torch.empty((units, K), dtype=torch.float32, device="cuda")
+        ids = torch.empty((units, K), dtype=torch.int32, device="cuda")
+        lcae.topk_init(vals, ids, stream.cuda_stream)
+
+        def step(i):
+            L.encode(pool[i % len(pool)], pooled, want_loss=False)
+            lcae.topk_update(pooled, vals, ids, i * shape.batch, stream.cuda_stream)
+        for i in range(args.warmup):
+            step(i)
+        torch.cuda.synchronize()
+        launches = L.last_launch_count() + 1
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        L.profile(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            for i in range(args.steps):
+                step(args.warmup + i)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        L.profile(False)
+        ms = e0.elapsed_time(e1)
+        kern_ms, kern_n = L.profile_read()
+        if dist:
+            t = torch.tensor([ms, kern_ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms, kern_ms = t.tolist()
+        # end to end: host batches (pinned) in, the top-K state's first unit read back each step
+        hosts = [pool[i].cpu().pin_memory() for i in range(2)]
+        probe = torch.empty((1, K), dtype=torch.float32).pin_memory()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        n_e2e = max(3, min(args.steps, 10))
+        for i in range(n_e2e):
+            L.encode(hosts[i % 2], pooled, want_loss=False)
+            lcae.topk_update(pooled, vals, ids, (1000 + i) * shape.batch, stream.cuda_stream)
+            probe.copy_(vals[:1], non_blocking=True)
+            stream.synchronize()
+        dt = (time.perf_counter() - t0) / n_e2e
+    if rank != 0:
+        return
+    ms_step = ms / args.steps
+    kern_avg = kern_ms / max(1, kern_n)
+    flops = 2.0 * shape.filters * shape.n * shape.batch * shape.fields   # encode U = W X
+    enc_bytes = 2.0 * shape.fields * 128 * shape.n + 6.0 * shape.batch * shape.img_h * shape.img_w * shape.img_c \
+        + 4.0 * shape.batch * units
+    achieved = flops / (kern_avg * 1e-3) / 1e12
+    achieved_gbs = enc_bytes / (kern_avg * 1e-3) / 1e9
+    hbm_bound = enc_bytes / (pk["hbm"] * 1e9) > flops / (pk["bf16_sus"] * 1e12)
+    line = {
+        "metric": INFER_METRIC, "value": world * shape.batch / (ms_step * 1e-3), "unit": "images/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": shape.name + "-infer", "image": [shape.img_h, shape.img_w, shape.img_c],
+                   "rf": shape.rf_h, "stride": shape.stride, "filters": shape.filters,
+                   "pool_group": shape.pool_group, "batch": shape.batch, "fields": shape.fields, "topk": K,
+                   "units": units, "parallelism": f"dp{world}" if world > 1 else "single"},
+        "roofline": ({"bound": "hbm", "achieved": achieved_gbs, "peak": pk["hbm"], "unit": "GB/s",
+                      "frac": achieved_gbs / pk["hbm"], "traffic": None, "kernel": "lcae::tc::step_kernel (encode)",
+                      "kernel_ms": kern_avg, "peak_source": f"{pk['src']} hbm_gbs"} if hbm_bound else
+                     {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
+                      "frac": achieved / pk["bf16_sus"], "traffic": None,
+                      "kernel": "lcae::tc::step_kernel (encode)", "kernel_ms": kern_avg,
+                      "peak_source": f"{pk['src']} bf16_tflops_sustained", "hbm_frac": achieved_gbs / pk["hbm"]}),
+        "gpu_launches": launches * args.steps,
+        "clocks": clk.summary(),
+        "e2e": {"value": world * shape.batch / dt, "unit": "images/s",
+                "h2d_bytes_per_step": hosts[0].numel() * 4, "d2h_bytes_per_step": K * 4, "ms_per_step": dt * 1e3},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_ours(args, shape):
     import torch
     from paper_1502_03409_b200 import lcae
@@ -300,6 +401,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of oracle work per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--momentum", type=float, default=0.0, help="SGD momentum (SURVEY.md §8(f) item 3: 0.9)")
+    ap.add_argument("--mode", default="train", choices=["train", "infer"],
+                    help="train: the training step (default); infer: encode + top-K stimuli (§8(f) item 4)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     shape = CONFIGS[args.config]
@@ -307,6 +410,8 @@ def main():
         shape = shape.replace(momentum=args.momentum)
     if args.impl == "reference":
         run_reference(args, shape)
+    elif args.mode == "infer":
+        run_infer(args, shape)
     else:
         run_ours(args, shape)
 

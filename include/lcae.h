@@ -112,6 +112,22 @@ lcae_status lcae_get_grads(lcae_layer *L, float *dW, float *dalpha, float *db);
  * call synchronises and returns LCAE_ERR_NUMERIC when J is not finite). x: host or device NHWC f32. */
 lcae_status lcae_forward(lcae_layer *L, const float *x, float *pooled, double *loss);
 
+/* Inference (SPEC.md:490 forward_dataset, "forward propagated 2 million
+ * images ... to obtain activation values"): the encode + L2-pooling half of the layer only (no decode, no
+ * update). pooled (required) receives p [m][grid_r][grid_c][k/g] (host or device); j_sparse (nullable,
+ * synchronises) receives lambda * sum p. Parameters are not modified. Errors: ARG, DATA, CUDA. */
+lcae_status lcae_encode(lcae_layer *L, const float *x, float *pooled, double *j_sparse);
+
+/* Streaming top-K stimuli per unit (SPEC.md:500-508 top_k_stimuli; "top 5 stimuli").
+ * State: vals [units][K] f32 and ids [units][K] int32 (device), each row sorted by value descending, ties
+ * by lower image id; lcae_topk_init fills it with (-inf, INT32_MAX). lcae_topk_update merges one batch of
+ * activations act [m][units] (device f32, e.g. the pooled output of lcae_encode with units =
+ * grid_r*grid_c*(k/g)) whose sample s has image id id0 + s. 1 <= K <= 32 (else LCAE_ERR_ARG). Ordered on
+ * `stream` (cudaStream_t; NULL = default stream); no synchronisation. */
+lcae_status lcae_topk_init(float *vals, int32_t *ids, int64_t units, int32_t K, void *stream);
+lcae_status lcae_topk_update(const float *act, int64_t m, int64_t units, int32_t K, int64_t id0, float *vals,
+                             int32_t *ids, void *stream);
+
 /* One training step on batch x (host or device NHWC f32): loss and gradients at the current parameters,
  * the input gradient dX overlap-added over fields into dx (nullable: the dX contraction still runs,
  * the result stays in the layer's device buffer — see lcae_dx_device), then the fused projected-SGD

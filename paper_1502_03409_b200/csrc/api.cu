@@ -273,14 +273,16 @@ lcae_status lcae_get_grads(lcae_layer *L, float *dW, float *dalpha, float *db) {
   return LCAE_OK;
 }
 
-static lcae_status run(lcae_layer *L, const float *x, bool update, float *dx, float *pooled, double *loss) {
+static lcae_status run(lcae_layer *L, const float *x, bool update, float *dx, float *pooled, double *loss,
+                       bool encode_only = false) {
   if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
   if (!x) { set_error("NULL input"); return LCAE_ERR_ARG; }
   L->launches = 0;
   const Geo &g = L->geo;
   lcae_status s;
   if ((s = stage_input(L, x))) return s;
-  s = (L->cfg.precision == LCAE_FP32) ? f32_step(L, update, pooled != nullptr) : tc_step(L, update, pooled != nullptr);
+  s = (L->cfg.precision == LCAE_FP32) ? f32_step(L, update, pooled != nullptr)
+                                       : tc_step(L, update, pooled != nullptr, encode_only);
   if (s) return s;
   if ((s = launch_loss_reduce(L))) return s;
   if (update) {
@@ -298,6 +300,13 @@ static lcae_status run(lcae_layer *L, const float *x, bool update, float *dx, fl
 
 lcae_status lcae_forward(lcae_layer *L, const float *x, float *pooled, double *loss) {
   return run(L, x, false, nullptr, pooled, loss);
+}
+
+lcae_status lcae_encode(lcae_layer *L, const float *x, float *pooled, double *j_sparse) {
+  if (!pooled) { set_error("lcae_encode: pooled output required"); return LCAE_ERR_ARG; }
+  lcae_status st = run(L, x, false, nullptr, pooled, nullptr, true);
+  if (st || !j_sparse) return st;
+  return lcae_last_loss(L, nullptr, j_sparse);   // the sparsity term (the fp32 path also forms J_rec)
 }
 
 lcae_status lcae_step(lcae_layer *L, const float *x, float *dx, double *loss) {

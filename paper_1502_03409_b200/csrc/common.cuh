@@ -129,7 +129,7 @@ lcae_status f32_step(lcae_layer *L, bool update, bool want_pooled);
 
 lcae_status tc_alloc(lcae_layer *L);
 void tc_free(lcae_layer *L);
-lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled);
+lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_only = false);
 double *tc_loss_part(lcae_layer *L);
 int tc_loss_count(lcae_layer *L);
 

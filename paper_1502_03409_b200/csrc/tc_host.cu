@@ -159,7 +159,7 @@ void tc_free(lcae_layer *L) {
   L->tc = nullptr;
 }
 
-lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled) {
+lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_only) {
   const Geo &g = L->geo;
   TcScratch *s = L->tc;
   tc::Params P;
@@ -172,7 +172,7 @@ lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled) {
   P.CB = s->CB;
   P.n_al = L->n_al;
   P.wp = L->wp;
-  P.mode = update ? 1 : 0;
+  P.mode = update ? 1 : (encode_only ? 2 : 0);
   P.dbg = getenv("LCAE_DEBUG_FLAGS") ? atoi(getenv("LCAE_DEBUG_FLAGS")) : 0;
   P.want_pooled = want_pooled ? 1 : 0;
   P.keep_grads = L->cfg.keep_grads;

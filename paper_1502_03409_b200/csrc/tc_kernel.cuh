@@ -86,7 +86,8 @@ struct __align__(1024) Smem {
   uint8_t Dl[2][16384];      // pass 0: X slots 2,3
   uint8_t negI[8192];        // -I (64 x 64 bf16, SW128)
   float recv[2][128][16];    // peer's dW partial for this CTA's owned 16-column chunks, [half][row][col]
-  float stg[NEPI][32][16];   // per-warp transpose staging of the own dW chunk (16-byte chunks swizzled)
+  float stg[NEPI][32][16];   // per-warp transpose staging of the own dW chunk (16-byte chunks swizzled);
+                             // forward / encode modes: recv + stg (contiguous) = 8 x 4 KB pooled-output staging
   uint16_t off[MAX_NPAD];    // pixel-feature offset of patch row n inside the field window (host-checked < 2^16)
   float bs[MAX_NPAD];        // b_f of the current field (epilogue)
   float sig[KP];
@@ -95,6 +96,7 @@ struct __align__(1024) Smem {
   float redf[NEPI];
   uint64_t wfull[NW], wempty[NW], xfull[NX], xempty[NX], p0full[NP0], p0empty[NP0], p1full[2], p1empty[2];
   uint64_t p0_ok, u_full, h_ready, g_full, d_ready, d_stored;
+  uint64_t uf[4], ue[4];     // encode-only mode: 4 U buffers in TMEM (full / free)
   uint64_t r_full[NRB], r_empty[NRB], dl_full[2], dl_empty[2];
   uint64_t p2_full[NB2], p2_empty[NB2], d2full[2], d2empty[2];
   uint64_t recv_full, peer_free;
@@ -106,6 +108,7 @@ struct __align__(1024) Smem {
 #define UCOMMIT_E(bar) do { if (ptx::elect_one()) ptx::umma_commit(bar); __syncwarp(); } while (0)
 
 static_assert(offsetof(Smem, bs) % 16 == 0, "float4 reads of b_f");
+static_assert(offsetof(Smem, stg) == offsetof(Smem, recv) + sizeof(Smem::recv), "recv + stg form one staging region");
 
 // pass 0 borrows every operand buffer the previous field's pass 2 is done with (all free at p0_ok)
 __device__ __forceinline__ uint8_t *p0slot(Smem &S, int i) {
@@ -172,6 +175,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
   const int s0 = (int)crank * MC;   // first sample of this CTA
   const int T = P.T, n = g.n, k = g.k, m = g.m, mp = P.mp;
   const bool step = P.mode == 1;
+  const bool enc = P.mode == 2;   // encode-only inference (pass 0 + pooling)
   // trace: lane 0 of the producers / MMA warp and of epilogue warp 2 record their barrier-wait cycles
   const bool trec = P.trace != nullptr && lane == 0 && (warp <= 2 || warp == XWARP);
   const long long t_start = clock64();
@@ -219,6 +223,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     ptx::mbar_init(&S.p0_ok, 1);
     for (int i = 0; i < NB2; ++i) { ptx::mbar_init(&S.p2_full[i], 1); ptx::mbar_init(&S.p2_empty[i], NEPI); }
     ptx::mbar_init(&S.u_full, 1);
+    for (int i = 0; i < 4; ++i) { ptx::mbar_init(&S.uf[i], 1); ptx::mbar_init(&S.ue[i], NEPI); }
     ptx::mbar_init(&S.h_ready, NEPI);
     ptx::mbar_init(&S.g_full, 1);
     ptx::mbar_init(&S.d_ready, NEPI);
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       ptx::tma_prefetch(&P.tmW);
       const uint64_t pol = ptx::policy_evict_first();   // W is streamed once per pass: keep X / dX in L2
       uint32_t q = 0;
-      const int npass = step ? 3 : 2;
+      const int npass = step ? 3 : (enc ? 1 : 2);
       for (int f = cid; f < g.F; f += ncl)
         for (int pass = 0; pass < npass; ++pass)
           for (int j = 0; j < T; ++j, ++q) {
@@ -319,6 +324,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         TWAIT(29, ptx::mbar_wait(&S.p0empty[s], ((q0 / NP0) & 1) ^ 1));
         load_tile(p0slot(S, s), &S.p0full[s], j);
       }
+      if (enc) continue;   // encode-only: the pass-0 ring's own barriers order the next field's loads
       // pass 1 ring lives in the D' buffer once the encode MMAs are done
       TWAIT(30, ptx::mbar_wait(&S.u_full, nf & 1));
       for (int j = 0; j < T; ++j, ++q1) {
@@ -385,7 +391,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         }
       };
       for (int f = cid; f < g.F; f += ncl, ++nf) {
-        // ---- pass 0: U^T = X^T W~^T
+        // ---- pass 0: U^T = X^T W~^T (encode-only: into one of 4 U buffers, so that the next fields' encodes
+        // overlap this field's pooling epilogue)
+        const uint32_t ucol = enc ? 128 * (nf & 3) : 384;
+        if (enc) {
+          TWAIT(2, ptx::mbar_wait(&S.ue[nf & 3], ((nf >> 2) & 1) ^ 1));
+          ptx::tc_fence_after();
+        }
         for (int j = 0; j < T; ++j, ++qw, ++q0) {
           wait_w(qw);
           TWAIT(1, ptx::mbar_wait(&S.p0full[q0 % NP0], (q0 / NP0) & 1));
@@ -396,10 +408,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           for (int kk = 0; kk < NT / 16; ++kk) {
             uint64_t ad = ptx::sdesc_sw128(xs + kk * 2048, 8192, 1024);
             uint64_t bd = ptx::sdesc_sw128(wst(qw) + kk * 32, 16, 1024);
-            UMMA_E(tb + 384, ad, bd, id_enc, (j | kk) != 0);
+            UMMA_E(tb + ucol, ad, bd, id_enc, (j | kk) != 0);
           }
           UCOMMIT_E(&S.wempty[qw % NW]);
           UCOMMIT_E(&S.p0empty[q0 % NP0]);
+        }
+        if (enc) {
+          UCOMMIT_E(&S.uf[nf & 3]);
+          continue;
         }
         UCOMMIT_E(&S.u_full);
         // ---- pass 1: R_j - X_j, then G += delta_{j-GLAG} W~_{j-GLAG}^T
@@ -518,42 +534,87 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       float dap = 0.f, rsq4[4] = {0.f, 0.f, 0.f, 0.f};   // rsq4[i]: row 8i + lane/4 of this warp
       TMARK(-1);
       // ------------------------------------------------ E0: pooling / sparsity, H' (filters [64 half, +64))
-      TWAIT(11, ptx::mbar_wait(&S.u_full, nf & 1));
+      const uint32_t ucol = enc ? 128 * (nf & 3) : 384;
+      if (enc) TWAIT(11, ptx::mbar_wait(&S.uf[nf & 3], (nf >> 2) & 1));
+      else TWAIT(11, ptx::mbar_wait(&S.u_full, nf & 1));
       ptx::tc_fence_after();
 #pragma unroll 1
       for (int cc = 2 * half; cc < 2 * half + 2; ++cc) {
         float u[32];
-        ptx::tmem_ld16(tl + 384 + cc * 32, u);
-        ptx::tmem_ld16(tl + 384 + cc * 32 + 16, u + 16);
+        ptx::tmem_ld16(tl + ucol + cc * 32, u);
+        ptx::tmem_ld16(tl + ucol + cc * 32 + 16, u + 16);
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int t = 0; t < 32; ++t) u[t] *= S.sig[cc * 32 + t];
+        constexpr int NGC = 32 / GP;   // pooling groups per 32-filter chunk
+        float pv[NGC];
 #pragma unroll
         for (int G0 = 0; G0 < 32; G0 += GP) {
           float ss = 0.f;
 #pragma unroll
           for (int t = 0; t < GP; ++t) { float h = a * u[G0 + t]; ss = fmaf(h, h, ss); }
           const int G = (cc * 32 + G0) / GP;
-          if (G < ng && svalid) {
-            const float v = P.eps + ss;
-            const float sG = v > 0.f ? v * rsqrtf(v) : 0.f;   // sqrt(eps + sum_G h^2)
-            js += (double)sG;
-            if (P.want_pooled) P.pooled[(((int64_t)gi * g.gr + fr) * g.gc + fc) * ng + G] = sG;
+          const float v = P.eps + ss;
+          const float sG = v > 0.f ? v * rsqrtf(v) : 0.f;   // sqrt(eps + sum_G h^2)
+          pv[G0 / GP] = sG;
+          if (G < ng && svalid) js += (double)sG;
+        }
+        if (P.want_pooled) {   // p [m][gr][gc][ng] (forward / encode only: recv + stg are idle then)
+          const int G0c = cc * NGC;   // first group of the chunk
+          if constexpr (NGC >= 4) {
+            // coalesced: the warp's 32 samples x NGC groups are transposed through 4 KB of staging so that
+            // each store instruction writes whole 16-byte runs of consecutive groups of a few samples
+            constexpr int NC4 = NGC / 4;
+            float *pst = &S.recv[0][0][0] + ew * 1024;   // recv and stg are contiguous: 8 x 4 KB
+#pragma unroll
+            for (int c4 = 0; c4 < NC4; ++c4)
+              *reinterpret_cast<float4 *>(pst + lane * NGC + 4 * (c4 ^ (lane % NC4))) =
+                  make_float4(pv[4 * c4], pv[4 * c4 + 1], pv[4 * c4 + 2], pv[4 * c4 + 3]);
+            __syncwarp();
+#pragma unroll
+            for (int e = lane; e < 32 * NC4; e += 32) {
+              const int r = e / NC4, c4 = e % NC4, gs = s0 + qd * 32 + r;
+              const float4 q = *reinterpret_cast<const float4 *>(pst + r * NGC + 4 * (c4 ^ (r % NC4)));
+              float *dst = P.pooled + (((int64_t)gs * g.gr + fr) * g.gc + fc) * ng + G0c + 4 * c4;
+              if (gs < m) {
+                if ((ng & 3) == 0) {   // 16-byte aligned rows
+                  if (G0c + 4 * c4 < ng) *reinterpret_cast<float4 *>(dst) = q;
+                } else {
+                  const float qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                  for (int e2 = 0; e2 < 4; ++e2)
+                    if (G0c + 4 * c4 + e2 < ng) dst[e2] = qq[e2];
+                }
+              }
+            }
+            __syncwarp();
+          } else {
+#pragma unroll
+            for (int q = 0; q < NGC; ++q)
+              if (G0c + q < ng && svalid) P.pooled[(((int64_t)gi * g.gr + fr) * g.gc + fc) * ng + G0c + q] = pv[q];
           }
         }
 #pragma unroll
         for (int t = 0; t < 32; ++t) u[t] = svalid ? S.sig[cc * 32 + t] * a * u[t] : 0.f;
         uint8_t *blk = S.H + (cc >> 1) * 16384;
+        if (!enc) {   // encode-only: H is a pass-0 X slot of the next field
 #pragma unroll
-        for (int t = 0; t < 32; t += 8) st8(blk, row, (cc & 1) * 32 + t, u + t);
+          for (int t = 0; t < 32; t += 8) st8(blk, row, (cc & 1) * 32 + t, u + t);
+        }
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&S.h_ready);
+      if (enc) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&S.ue[nf & 3]);   // U buffer read: the MMA may encode into it again
+      } else if (lane == 0) {
+        ptx::mbar_arrive(&S.h_ready);
+      }
       TMARK(32);
       // ------------------------------------------------ E1: residual, delta, db (pass 1)
 #pragma unroll 1
-      for (int j = 0; j < T; ++j, ++ur) {
+      for (int j = 0; j < (enc ? 0 : T); ++j, ++ur) {
         const uint32_t rb = ur % NRB;
         if (j == 0) TWAIT(43, ptx::mbar_wait(&S.r_full[rb], (ur / NRB) & 1));
         else TWAIT(12, ptx::mbar_wait(&S.r_full[rb], (ur / NRB) & 1));

@@ -52,6 +52,9 @@ def _load():
         "lcae_get_grads": (C.c_int, [P, P, P, P]),
         "lcae_forward": (C.c_int, [P, P, P, C.POINTER(C.c_double)]),
         "lcae_step": (C.c_int, [P, P, P, C.POINTER(C.c_double)]),
+        "lcae_encode": (C.c_int, [P, P, P, C.POINTER(C.c_double)]),
+        "lcae_topk_init": (C.c_int, [P, P, C.c_int64, C.c_int32, P]),
+        "lcae_topk_update": (C.c_int, [P, C.c_int64, C.c_int64, C.c_int32, C.c_int64, P, P, P]),
         "lcae_last_loss": (C.c_int, [P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "lcae_dx_device": (C.c_int, [P, C.POINTER(P)]),
         "lcae_counters": (C.c_int, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -80,7 +83,8 @@ lib = _load()
 
 # Every symbol include/lcae.h declares (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("lcae_config_default", "lcae_geometry", "lcae_create", "lcae_destroy", "lcae_set_params",
-               "lcae_get_params", "lcae_get_grads", "lcae_forward", "lcae_step", "lcae_last_loss",
+               "lcae_get_params", "lcae_get_grads", "lcae_forward", "lcae_encode", "lcae_step", "lcae_last_loss",
+               "lcae_topk_init", "lcae_topk_update",
                "lcae_dx_device", "lcae_counters", "lcae_region_add", "lcae_last_launch_count",
                "lcae_profile", "lcae_profile_read",
                "lcae_last_error", "lcae_version")
@@ -172,6 +176,12 @@ class Layer:
         check(lib.lcae_forward(self.h, _ptr(x), _ptr(pooled), C.byref(loss) if want_loss else None))
         return loss.value if want_loss else None
 
+    def encode(self, x, pooled, want_loss=True):
+        """Inference: encode + L2 pooling only (lcae_encode); returns J_sparse if want_loss."""
+        loss = C.c_double(0.0)
+        check(lib.lcae_encode(self.h, _ptr(x), _ptr(pooled), C.byref(loss) if want_loss else None))
+        return loss.value if want_loss else None
+
     def last_loss(self):
         a, b = C.c_double(), C.c_double()
         check(lib.lcae_last_loss(self.h, C.byref(a), C.byref(b)))
@@ -204,3 +214,16 @@ def region_add(dst, src, y0: int, x0: int, stream=None):
     m, dh, dw, Cc = dst.shape
     _, rows, cols, _ = src.shape
     check(lib.lcae_region_add(stream, _ptr(dst), dh, dw, _ptr(src), m, rows, cols, Cc, y0, x0))
+
+
+def topk_init(vals, ids, stream=None):
+    """Reset a streaming top-K state: vals float32 [units][K], ids int32 [units][K] (CUDA tensors)."""
+    units, K = vals.shape
+    check(lib.lcae_topk_init(vals.data_ptr(), ids.data_ptr(), units, K, stream))
+
+
+def topk_update(act, vals, ids, id0, stream=None):
+    """Merge one batch of activations act float32 [m][units] (CUDA) whose sample s is image id0 + s."""
+    m, units = act.shape[0], vals.shape[0]
+    check(lib.lcae_topk_update(act.data_ptr(), m, units, vals.shape[1], id0, vals.data_ptr(), ids.data_ptr(), stream))
+

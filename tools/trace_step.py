@@ -21,6 +21,7 @@ NAMES = {0: "mma:wfull", 1: "mma:p0full", 2: "mma:tmem_free", 3: "mma:h_ready", 
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+mode = sys.argv[3] if len(sys.argv) > 3 else "step"
 shape = CONFIGS[cfg_name]
 lib = lcae.lib
 lib.lcae_dev_trace.restype = C.c_int
@@ -29,13 +30,23 @@ L = lcae.Layer(lcae.make_config(shape, precision=lcae.BF16))
 W, a, b = make_params(shape, seed=0)
 L.set_params(W, a, b)
 x = torch.from_numpy(make_images(shape, seed=1)).cuda()
+pooled = torch.empty((shape.batch, shape.fields * (shape.filters // shape.pool_group)), device="cuda")
+
+
+def run():
+    if mode == "encode":
+        L.encode(x, pooled, want_loss=False)
+    else:
+        L.step(x, None, want_loss=False)
+
+
 for _ in range(2):
-    L.step(x, None, want_loss=False)
+    run()
 torch.cuda.synchronize()
 lcae.check(lib.lcae_dev_trace(L.h, 1, None))
 L.profile(True)
 for _ in range(steps):
-    L.step(x, None, want_loss=False)
+    run()
 torch.cuda.synchronize()
 ms, nl = L.profile_read()
 out = (C.c_ulonglong * 48)()
