@@ -128,6 +128,15 @@ lcae_status lcae_topk_init(float *vals, int32_t *ids, int64_t units, int32_t K, 
 lcae_status lcae_topk_update(const float *act, int64_t m, int64_t units, int32_t K, int64_t id0, float *vals,
                              int32_t *ids, void *stream);
 
+/* Local contrast normalisation of a layer output before the next layer (PAPER.md:95
+ * "local contrast normalization (LCN) is applied prior to continuing onto the next layer"; formula
+ * SPEC.md:215-223): v = x - mean_w(x), y = v / max(floor, sqrt(mean_w(v^2))), uniform window x window per
+ * channel, zero padding with count-correct divisors. x, y: device f32 [m][H][W][C] (y may not alias x);
+ * scratch: device f32, 2 m H W C elements. window odd and <= H, W; floor > 0 (else LCAE_ERR_CONFIG).
+ * Ordered on `stream`; no synchronisation. */
+lcae_status lcae_lcn(const float *x, float *y, float *scratch, int32_t m, int32_t H, int32_t W, int32_t C,
+                     int32_t window, float floor_, void *stream);
+
 /* One training step on batch x (host or device NHWC f32): loss and gradients at the current parameters,
  * the input gradient dX overlap-added over fields into dx (nullable: the dX contraction still runs,
  * the result stays in the layer's device buffer — see lcae_dx_device), then the fused projected-SGD

@@ -54,6 +54,7 @@ def _load():
         "lcae_step": (C.c_int, [P, P, P, C.POINTER(C.c_double)]),
         "lcae_encode": (C.c_int, [P, P, P, C.POINTER(C.c_double)]),
         "lcae_topk_init": (C.c_int, [P, P, C.c_int64, C.c_int32, P]),
+        "lcae_lcn": (C.c_int, [P, P, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, P]),
         "lcae_topk_update": (C.c_int, [P, C.c_int64, C.c_int64, C.c_int32, C.c_int64, P, P, P]),
         "lcae_last_loss": (C.c_int, [P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "lcae_dx_device": (C.c_int, [P, C.POINTER(P)]),
@@ -84,7 +85,7 @@ lib = _load()
 # Every symbol include/lcae.h declares (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("lcae_config_default", "lcae_geometry", "lcae_create", "lcae_destroy", "lcae_set_params",
                "lcae_get_params", "lcae_get_grads", "lcae_forward", "lcae_encode", "lcae_step", "lcae_last_loss",
-               "lcae_topk_init", "lcae_topk_update",
+               "lcae_topk_init", "lcae_topk_update", "lcae_lcn",
                "lcae_dx_device", "lcae_counters", "lcae_region_add", "lcae_last_launch_count",
                "lcae_profile", "lcae_profile_read",
                "lcae_last_error", "lcae_version")
@@ -226,4 +227,11 @@ def topk_update(act, vals, ids, id0, stream=None):
     """Merge one batch of activations act float32 [m][units] (CUDA) whose sample s is image id0 + s."""
     m, units = act.shape[0], vals.shape[0]
     check(lib.lcae_topk_update(act.data_ptr(), m, units, vals.shape[1], id0, vals.data_ptr(), ids.data_ptr(), stream))
+
+
+def lcn(x, y, scratch, window=9, floor=1e-4, stream=None):
+    """Local contrast normalisation (lcae_lcn): x, y float32 CUDA [m][H][W][C], scratch >= 2 x.numel()."""
+    m, H, W, Cc = x.shape
+    assert scratch.numel() >= 2 * x.numel()
+    check(lib.lcae_lcn(x.data_ptr(), y.data_ptr(), scratch.data_ptr(), m, H, W, Cc, window, floor, stream))
 
