@@ -29,7 +29,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-from paper_1502_03409_b200.inputs import CONFIGS, make_images, make_params, stratified_fields  # noqa: E402
+from paper_1502_03409_b200.inputs import CONFIGS, LayerShape, make_images, make_params, stratified_fields  # noqa: E402
 
 METRIC = "images/sec per LC-autoencoder training step"
 
@@ -271,6 +271,13 @@ def run_infer(args, shape):
     print(json.dumps(line), flush=True)
 
 
+# SURVEY.md §8(d) c5 "15 B point": the paper's parameter count ("15 billion parameters") as one
+# c3-shaped layer, 347 x 348 fields of 18 x 18 x 3 -> 128 filters (15.02 B weights), batch 256, on ONE GPU
+# (fp32 master + bf16 shadow ~ 6 B/param = 90 GB of the 180 GB HBM). Weights are initialised on the device.
+EXTRA = {"c15b": LayerShape("c15b", 710, 712, 3, 18, 18, 2, 128, 1, 256)}
+DEVICE_INIT_PARAMS = 4e9   # above this many weights the host never materialises W (lcae_create seeds them)
+
+
 def run_ours(args, shape):
     import torch
     from paper_1502_03409_b200 import lcae
@@ -292,9 +299,10 @@ def run_ours(args, shape):
         if world == 1:
             cfg = lcae.make_config(shape, precision=lcae.BF16, stream=stream.cuda_stream)
             L = lcae.Layer(cfg)
-            W, a, b = make_params(shape, seed=0)
-            L.set_params(W, a, b)
-            del W
+            if shape.fields * shape.filters * shape.n < DEVICE_INIT_PARAMS:
+                W, a, b = make_params(shape, seed=0)
+                L.set_params(W, a, b)
+                del W
             pool = [torch.from_numpy(make_images(shape, seed=1, index=i)).cuda() for i in range(4)]
             step = lambda i: L.step(pool[i % len(pool)], None, want_loss=False)  # noqa: E731
         else:
@@ -396,7 +404,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + sorted(EXTRA))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of oracle work per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -405,7 +413,7 @@ def main():
                     help="train: the training step (default); infer: encode + top-K stimuli (§8(f) item 4)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
-    shape = CONFIGS[args.config]
+    shape = CONFIGS[args.config] if args.config in CONFIGS else EXTRA[args.config]
     if args.momentum:
         shape = shape.replace(momentum=args.momentum)
     if args.impl == "reference":
