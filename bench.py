@@ -274,7 +274,7 @@ def run_infer(args, shape):
 # SURVEY.md §8(d) c5 "15 B point": the paper's parameter count ("15 billion parameters") as one
 # c3-shaped layer, 347 x 348 fields of 18 x 18 x 3 -> 128 filters (15.02 B weights), batch 256, on ONE GPU
 # (fp32 master + bf16 shadow ~ 6 B/param = 90 GB of the 180 GB HBM). Weights are initialised on the device.
-EXTRA = {"c15b": LayerShape("c15b", 710, 712, 3, 18, 18, 2, 128, 1, 256)}
+EXTRA = {"c15b": LayerShape("c15b", 710, 712, 3, 18, 18, 2, 128, 1, 256, lr=1e-3 / 256)}
 DEVICE_INIT_PARAMS = 4e9   # above this many weights the host never materialises W (lcae_create seeds them)
 
 
@@ -305,6 +305,16 @@ def run_ours(args, shape):
                 del W
             pool = [torch.from_numpy(make_images(shape, seed=1, index=i)).cuda() for i in range(4)]
             step = lambda i: L.step(pool[i % len(pool)], None, want_loss=False)  # noqa: E731
+            if args.graph:   # one CUDA graph per pool entry (launch-bound small configs)
+                torch.cuda.synchronize()
+                graphs = []
+                for xi in pool:
+                    gph = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(gph, stream=stream):
+                        L.step(xi, None, want_loss=False)
+                    graphs.append(gph)
+                eager_step = step
+                step = lambda i: graphs[i % len(graphs)].replay()  # noqa: E731
         else:
             L = runner.layer
             step = runner.bench_step_fn(stream)
@@ -330,6 +340,13 @@ def run_ours(args, shape):
         L.profile(False)
         ms = e0.elapsed_time(e1)
         kern_ms, kern_n = L.profile_read()
+        if world == 1 and args.graph:   # graph replays carry no profile events: time the kernel on eager steps
+            L.profile(True)
+            for i in range(10):
+                eager_step(i)
+            torch.cuda.synchronize()
+            L.profile(False)
+            kern_ms, kern_n = L.profile_read()
         if dist:
             t = torch.tensor([ms, kern_ms], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -373,7 +390,7 @@ def run_ours(args, shape):
         "config": {"workload": shape.name, "image": [shape.img_h, shape.img_w, shape.img_c], "rf": shape.rf_h,
                    "stride": shape.stride, "filters": shape.filters, "pool_group": shape.pool_group,
                    "batch": shape.batch, "fields": shape.fields, "params": shape.fields * shape.filters * shape.n,
-                   "momentum": shape.momentum,
+                   "momentum": shape.momentum, "cuda_graph": bool(args.graph),
                    "parallelism": f"mp{world}" if world > 1 else "single",
                    "l2": "working set > L2 (fp32 W master 4 B/param streamed every step)"},
         "tflops": flops / (ms_step * 1e-3) / 1e12,
@@ -409,6 +426,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of oracle work per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--momentum", type=float, default=0.0, help="SGD momentum (SURVEY.md §8(f) item 3: 0.9)")
+    ap.add_argument("--graph", action="store_true", help="replay each step from a captured CUDA graph (1 GPU)")
     ap.add_argument("--mode", default="train", choices=["train", "infer"],
                     help="train: the training step (default); infer: encode + top-K stimuli (§8(f) item 4)")
     args = ap.parse_args()

@@ -128,7 +128,7 @@ lcae_status lcae_destroy(lcae_layer *L) {
   for (void *p : {(void *)L->W, (void *)L->sigma, (void *)L->alpha, (void *)L->b, (void *)L->vW, (void *)L->va,
                   (void *)L->vb, (void *)L->Wb, (void *)L->x_stage, (void *)L->xt32, (void *)L->xt16,
                   (void *)L->dxt, (void *)L->dx_nhwc, (void *)L->pooled, (void *)L->gW, (void *)L->galpha,
-                  (void *)L->gb, (void *)L->loss_part, (void *)L->loss_dev, (void *)L->reinit_dev,
+                  (void *)L->gb, (void *)L->loss_part, (void *)L->loss_dev, (void *)L->reinit_dev, (void *)L->step_dev,
                   (void *)L->rowsq})
     if (p) cudaFree(p);
   if (L->loss_host) cudaFreeHost(L->loss_host);
@@ -195,6 +195,8 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
   CKF(cudaMemsetAsync(L->loss_dev, 0, 2 * sizeof(double), L->st));
   CKF(cudaMalloc(&L->reinit_dev, sizeof(int)));
   CKF(cudaMemsetAsync(L->reinit_dev, 0, sizeof(int), L->st));
+  CKF(cudaMalloc(&L->step_dev, sizeof(int64_t)));
+  CKF(cudaMemsetAsync(L->step_dev, 0, sizeof(int64_t), L->st));
   CKF(cudaMallocHost(&L->loss_host, 2 * sizeof(double)));
   if (cfg->keep_grads) {
     CKF(cudaMalloc(&L->gW, F * k * wp * 4));
@@ -284,7 +286,7 @@ static lcae_status run(lcae_layer *L, const float *x, bool update, float *dx, fl
   s = (L->cfg.precision == LCAE_FP32) ? f32_step(L, update, pooled != nullptr)
                                        : tc_step(L, update, pooled != nullptr, encode_only);
   if (s) return s;
-  if ((s = launch_loss_reduce(L))) return s;
+  if ((s = launch_loss_reduce(L, update))) return s;
   if (update) {
     if ((s = launch_hwcn_to_nhwc_f32(L, L->dxt, L->dx_nhwc))) return s;
     if (dx && (s = copy_any(L, dx, L->dx_nhwc, (size_t)g.m * g.H * g.W * g.C * 4))) return s;
@@ -331,9 +333,11 @@ lcae_status lcae_dx_device(lcae_layer *L, float **dx_dev) {
 lcae_status lcae_counters(lcae_layer *L, int64_t *steps, int64_t *reinit_rows) {
   if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
   int r = 0;
+  int64_t st = 0;
   LCAE_CK(cudaMemcpyAsync(&r, L->reinit_dev, sizeof(int), cudaMemcpyDeviceToHost, L->st));
+  LCAE_CK(cudaMemcpyAsync(&st, L->step_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, L->st));
   LCAE_CK(cudaStreamSynchronize(L->st));
-  if (steps) *steps = L->steps;
+  if (steps) *steps = st;
   if (reinit_rows) *reinit_rows = r;
   return LCAE_OK;
 }

@@ -46,14 +46,19 @@ __global__ void hwcn_to_nhwc(const float *__restrict__ xt, float *__restrict__ x
 }
 
 // Fixed-order fp64 reduction of the per-field loss partials [F][2] -> loss[2].
-__global__ void __launch_bounds__(1024) loss_reduce(const double *part, int F, double *out) {  // F = #partial pairs
+__global__ void __launch_bounds__(1024) loss_reduce(const double *part, int F, double *out, int64_t *step_dev,
+                                                    int update) {  // F = #partial pairs
   __shared__ double sh[32];
   double a = 0.0, b = 0.0;
   for (int f = threadIdx.x; f < F; f += blockDim.x) { a += part[2 * f]; b += part[2 * f + 1]; }
   double ta = block_sum_f64(a, sh);
   __syncthreads();
   double tb = block_sum_f64(b, sh);
-  if (threadIdx.x == 0) { out[0] = ta; out[1] = tb; }
+  if (threadIdx.x == 0) {
+    out[0] = ta;
+    out[1] = tb;
+    if (update) ++*step_dev;   // after this step's finalize (stream order), before the next step's
+  }
 }
 
 // Default init: counter-based uniform rows (unit length), alpha = alpha_init, b = 0, sigma = 1.
@@ -146,10 +151,10 @@ lcae_status launch_hwcn_to_nhwc_f32(lcae_layer *L, const float *xt, float *x) {
   return LCAE_OK;
 }
 
-lcae_status launch_loss_reduce(lcae_layer *L) {
+lcae_status launch_loss_reduce(lcae_layer *L, bool update) {
   const bool tcp = L->cfg.precision == LCAE_BF16;
   loss_reduce<<<1, 1024, 0, L->st>>>(tcp ? tc_loss_part(L) : L->loss_part, tcp ? tc_loss_count(L) : L->geo.F,
-                                     L->loss_dev);
+                                     L->loss_dev, L->step_dev, update ? 1 : 0);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }

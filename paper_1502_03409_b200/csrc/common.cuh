@@ -78,6 +78,7 @@ struct lcae_layer {
   // loss: per-field partials [F][2] fp64 (rec, sparse) and the reduced pair
   double *loss_part = nullptr, *loss_dev = nullptr, *loss_host = nullptr;
   int *reinit_dev = nullptr;   // degenerate rows re-initialised (device counter)
+  int64_t *step_dev = nullptr;   // steps taken (device counter: CUDA-graph replays stay exact)
   float *rowsq = nullptr;      // [F][k] row sums of squares of the updated W~ (bf16 mode)
   int64_t steps = 0;
   int launches = 0;
@@ -137,7 +138,7 @@ int tc_loss_count(lcae_layer *L);
 lcae_status launch_nhwc_to_hwcn_f32(lcae_layer *L, const float *x, float *xt);
 lcae_status launch_nhwc_to_hwcn_bf16(lcae_layer *L, const float *x, __nv_bfloat16 *xt);
 lcae_status launch_hwcn_to_nhwc_f32(lcae_layer *L, const float *xt, float *x);
-lcae_status launch_loss_reduce(lcae_layer *L);
+lcae_status launch_loss_reduce(lcae_layer *L, bool update);
 lcae_status launch_init_params(lcae_layer *L);
 lcae_status launch_fill(lcae_layer *L, float *p, int64_t n, float v);
 lcae_status launch_get_W(lcae_layer *L, float *Wout);   // sigma (.) W~ -> dense [F][k][n]

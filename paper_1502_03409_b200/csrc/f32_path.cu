@@ -206,7 +206,7 @@ __global__ void col2im_f32(Geo g, int f0, int Fc, const float *dXp, float *dxt) 
 // Projected SGD on W rows (fp32 mode keeps W normalised, sigma == 1):
 // v = mu v - lr dW; W' = W + v; W' /= ||W'|| (degenerate rows re-initialised).
 __global__ void __launch_bounds__(256) update_w_f32(Geo g, int f0, float *W, const float *dW, float *vW, float lr,
-                                                    float mu, uint64_t seed, int64_t step, int row0, int col0,
+                                                    float mu, uint64_t seed, const int64_t *step_dev, int row0, int col0,
                                                     int ggc, int *reinit) {
   __shared__ double sh[32];
   __shared__ float s_scale;
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256) update_w_f32(Geo g, int f0, float *W, con
   if (sc < 0.f) {   // degenerate row: deterministic counter-based re-initialisation
     int r = f / g.gc, c = f - r * g.gc;
     uint64_t gf = (uint64_t)((row0 + r) * ggc + col0 + c);
-    uint64_t key = splitmix64(seed ^ ((uint64_t)step << 40) ^ (gf << 20) ^ (uint64_t)j);
+    uint64_t key = splitmix64(seed ^ ((uint64_t)*step_dev << 40) ^ (gf << 20) ^ (uint64_t)j);
     double a2 = 0.0;
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
       double u = (double)(splitmix64(key + (uint64_t)t) >> 40) / 16777216.0 - 0.5;
@@ -341,7 +341,7 @@ lcae_status f32_step(lcae_layer *L, bool update, bool want_pooled) {
     }
     // projected SGD update of this chunk's fields
     update_w_f32<<<dim3(Fc, k), 256, 0, L->st>>>(g, f0, L->W, s.dW, L->vW, L->cfg.lr, L->cfg.momentum, L->cfg.seed,
-                                                 L->steps, L->cfg.field_row0, L->cfg.field_col0,
+                                                 L->step_dev, L->cfg.field_row0, L->cfg.field_col0,
                                                  L->cfg.global_grid_c, L->reinit_dev);
     LCAE_CK_LAUNCH(L);
     update_ab_f32<<<256, 256, 0, L->st>>>(g, f0, Fc, L->alpha, L->b, s.da, s.db, L->va, L->vb, L->cfg.lr,

@@ -14,7 +14,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(Geo g, int CB, int n_al, 
                                                        const float *db_part, const float *rowsq_part, float *alpha,
                                                        float *bvec, float *sigma, float *W, __nv_bfloat16 *Wb,
                                                        float *va, float *vb, float lr, float mu, float amin,
-                                                       float *galpha, float *gb, uint64_t seed, int64_t step,
+                                                       float *galpha, float *gb, uint64_t seed, const int64_t *step_dev,
                                                        int row0, int col0, int ggc, int *reinit) {
   __shared__ double sh[32];
   __shared__ int bad[KP];
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(Geo g, int CB, int n_al, 
     const int r = bad[ib];
     const int fr = f / g.gc, fc = f - fr * g.gc;
     const uint64_t gf = (uint64_t)((row0 + fr) * ggc + col0 + fc);
-    const uint64_t key = splitmix64(seed ^ ((uint64_t)step << 40) ^ (gf << 20) ^ (uint64_t)r);
+    const uint64_t key = splitmix64(seed ^ ((uint64_t)*step_dev << 40) ^ (gf << 20) ^ (uint64_t)r);
     double a2 = 0.0;
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
       double u = (double)(splitmix64(key + (uint64_t)t) >> 40) / 16777216.0 - 0.5;
@@ -226,7 +226,7 @@ lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_on
     tc::finalize_kernel<<<g.F, 128, 0, L->st>>>(
         g, s->CB, L->n_al, s->da_part, s->db_part, s->rowsq_part, L->alpha, L->b, L->sigma, L->W, L->Wb, L->va,
         L->vb, L->cfg.lr, L->cfg.momentum, L->cfg.alpha_min, L->cfg.keep_grads ? L->galpha : nullptr,
-        L->cfg.keep_grads ? L->gb : nullptr, L->cfg.seed, L->steps, L->cfg.field_row0, L->cfg.field_col0,
+        L->cfg.keep_grads ? L->gb : nullptr, L->cfg.seed, L->step_dev, L->cfg.field_row0, L->cfg.field_col0,
         L->cfg.global_grid_c, L->reinit_dev);
     LCAE_CK_LAUNCH(L);
   }

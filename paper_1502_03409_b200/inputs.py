@@ -66,10 +66,12 @@ class LayerShape:
 
 
 # BASELINE.json "configs" (SURVEY.md §8 shape table; R8: config 3 stride 2).
+# lr = 1e-3 / m (R19): the objective sums over the batch (R6), so SPEC.md:141's lr = 1e-3 is the
+# per-sample step; with it c2 / c3 diverge within 50 steps (alpha blows up), with 1e-3 / m they descend.
 CONFIGS = {
-    "c1": LayerShape("c1", 32, 32, 1, 8, 8, 4, 16, 2, 8),
-    "c2": LayerShape("c2", 96, 96, 3, 16, 16, 8, 64, 4, 128),
-    "c3": LayerShape("c3", 200, 200, 3, 18, 18, 2, 128, 1, 256),
+    "c1": LayerShape("c1", 32, 32, 1, 8, 8, 4, 16, 2, 8, lr=1e-3 / 8),
+    "c2": LayerShape("c2", 96, 96, 3, 16, 16, 8, 64, 4, 128, lr=1e-3 / 128),
+    "c3": LayerShape("c3", 200, 200, 3, 18, 18, 2, 128, 1, 256, lr=1e-3 / 256),
 }
 
 

@@ -15,9 +15,11 @@ pytestmark = pytest.mark.gpu
 
 TOL = {0: 1e-5, 1: 2e-2}
 
+# single-step parity at SPEC.md:141's lr = 1e-3 (the configs' bench lr is 1e-3 / m, R19): the update
+# is compared as theta' - theta, and at lr / m the fp32 rounding of theta' itself is ~1e-5 of that difference
 SHAPES = {
-    "c1": CONFIGS["c1"],
-    "c2": CONFIGS["c2"],
+    "c1": CONFIGS["c1"].replace(lr=1e-3),
+    "c2": CONFIGS["c2"].replace(lr=1e-3),
     # ragged: n = 5*7*2 = 70 (not a multiple of 16/64), k = 24, g = 4, odd batch, non-square image
     "ragged": LayerShape("ragged", 21, 25, 2, 5, 7, 2, 24, 4, 37),
     "worked": LayerShape("worked", 2, 1, 1, 2, 1, 1, 2, 1, 1, eps=0.0),
@@ -70,9 +72,9 @@ def test_fp32_parity(name):
 
 SHAPES_BF16 = {
     "worked": SHAPES["worked"],
-    "c1": CONFIGS["c1"],
+    "c1": SHAPES["c1"],
     "ragged": SHAPES["ragged"],
-    "c2": CONFIGS["c2"],
+    "c2": SHAPES["c2"],
     # two-CTA cluster (m > 128, ragged second slice), pooling g = 2, n = 8*8*3 = 192
     "cluster2": LayerShape("cluster2", 20, 20, 3, 8, 8, 4, 32, 2, 200),
     # paper layer-1-like field shape (k = 128, g = 1) on a small image, two CTAs
