@@ -147,6 +147,10 @@ __device__ __forceinline__ void red_v4_if(float *p, float a, float b, float c, f
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t@p red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
       "f"(a), "f"(b), "f"(c), "f"(d), "r"((int)pred));
 }
+// Invalidate one 128-byte L2 line without writing it back (dead scratch data).
+__device__ __forceinline__ void discard_l2(const void *p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
 // Bulk copy shared -> global (bulk-group completion; bytes multiple of 16).
 __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)

@@ -342,9 +342,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       TWAIT(28, ptx::mbar_wait(&S.g_full, nf & 1));
       ptx::fence_proxy_async_global();
       const uint8_t *dsrc = P.dscr + (size_t)blockIdx.x * T * 16384;
+      // a reloaded delta tile is dead once its MMAs completed (d2empty): its scratch lines are discarded from
+      // L2 so they are never written back to HBM (the next field's store-out rewrites them much later)
+      auto discard_tile = [&](int jj) {
+#pragma unroll
+        for (int l4 = 0; l4 < 4; ++l4) ptx::discard_l2(dsrc + (size_t)jj * 16384 + (size_t)(l4 * 32 + lane) * 128);
+        ptx::fence_proxy_async_global();   // ordered before the (async-proxy) bulk stores that rewrite the lines
+      };
       for (int j = 0; j < T; ++j, ++qx, ++qd2) {
         const int sd = qd2 & 1;
         TWAIT(31, ptx::mbar_wait(&S.d2empty[sd], ((qd2 >> 1) & 1) ^ 1));
+        if (j >= 2) discard_tile(j - 2);
         if (lane == 0) {
           ptx::mbar_arrive_expect_tx(&S.d2full[sd], 16384);
           ptx::bulk_g2s(S.Dl[sd], dsrc + (size_t)j * 16384, 16384, &S.d2full[sd]);
@@ -353,6 +361,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         const int s = qx % NX;
         TWAIT(31, ptx::mbar_wait(&S.xempty[s], ((qx / NX) & 1) ^ 1));
         load_tile(S.Xr[s], &S.xfull[s], j);
+      }
+      for (int j = std::max(0, T - 2); j < T; ++j) {   // the field's last two reloads: wait for their MMAs
+        const uint32_t qq = qd2 - T + j;
+        ptx::mbar_wait(&S.d2empty[qq & 1], (qq >> 1) & 1);
+        discard_tile(j);
       }
     }
   } else if (warp == 1) {
