@@ -530,6 +530,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     const int ng = k / GP;
     const int hc = 32 * half;             // first column of this warp within a tile
     uint32_t nf = 0, ur = 0, ud = 0, u2 = 0;
+    // cluster-peer addresses of the dW exchange, mapped once (mapa is an MIO round trip)
+    const uint32_t peer_recv = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.recv[half][row][0]), crank ^ 1u) : 0u;
+    const uint32_t peer_recv_full = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.recv_full), crank ^ 1u) : 0u;
+    const uint32_t peer_free_bar = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.peer_free), crank ^ 1u) : 0u;
     for (int f = cid; f < g.F; f += ncl, ++nf) {
       const int fr = f / g.gc, fc = f - fr * g.gc;
       const int64_t pixbase = ((int64_t)fr * g.s * g.W + (int64_t)fc * g.s) * g.C;
@@ -786,8 +790,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             // arm this tile's receive phase: 8 warps x 32 rows x 16 floats arrive from the peer via st.async
             if (etid == 0) ptx::mbar_arrive_expect_tx(&S.recv_full, 2 * 128 * 16 * 4);
             TWAIT(22, ptx::mbar_wait(&S.peer_free, (u2 & 1) ^ 1));
-            const uint32_t rdst = ptx::mapa(ptx::smem_u32(&S.recv[half][row][0]), peer);
-            const uint32_t rbar = ptx::mapa(ptx::smem_u32(&S.recv_full), peer);
+            const uint32_t rdst = peer_recv, rbar = peer_recv_full;
 #pragma unroll
             for (int t = 0; t < 4; ++t)
               ptx::st_async_v4(rdst + 16 * (t ^ swr),
@@ -819,7 +822,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             }
             __syncwarp();
             if (lane == 0)   // receive slice read: the peer may send the next tile (reads only; relaxed suffices)
-              ptx::mbar_arrive_remote_relaxed(ptx::mapa(ptx::smem_u32(&S.peer_free), crank ^ 1u));
+              ptx::mbar_arrive_remote_relaxed(peer_free_bar);
           }
           TMARK(42);
           if (do_sgd) {
