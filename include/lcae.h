@@ -137,6 +137,13 @@ lcae_status lcae_topk_update(const float *act, int64_t m, int64_t units, int32_t
 lcae_status lcae_lcn(const float *x, float *y, float *scratch, int32_t m, int32_t H, int32_t W, int32_t C,
                      int32_t window, float floor_, void *stream);
 
+/* Start copying the NEXT batch (a host NHWC f32 pointer; pinned memory for a truly asynchronous copy) into
+ * a device buffer on the layer's own copy stream, so that the transfer overlaps the current step; the
+ * lcae_step / lcae_forward / lcae_encode call that is given the same pointer then waits for that copy
+ * instead of copying. The host buffer must stay unchanged until that call. Device pointers are a no-op.
+ * Errors: ARG, CUDA. */
+lcae_status lcae_prefetch_input(lcae_layer *L, const float *x_host);
+
 /* One training step on batch x (host or device NHWC f32): loss and gradients at the current parameters,
  * the input gradient dX overlap-added over fields into dx (nullable: the dX contraction still runs,
  * the result stays in the layer's device buffer — see lcae_dx_device), then the fused projected-SGD

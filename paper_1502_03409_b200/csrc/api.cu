@@ -66,13 +66,20 @@ static lcae_status stage_input(lcae_layer *L, const float *x) {
   const Geo &g = L->geo;
   size_t bytes = (size_t)g.m * g.H * g.W * g.C * 4;
   const float *xd = x;
-  if (!is_device_ptr(x)) {
+  if (L->pf_host && L->pf_host == (const void *)x) {   // prefetched by lcae_prefetch_input
+    LCAE_CK(cudaStreamWaitEvent(L->st, L->pf_done, 0));
+    xd = L->x_pf;
+    L->pf_host = nullptr;
+  } else if (!is_device_ptr(x)) {
     lcae_status s = copy_any(L, L->x_stage, x, bytes);
     if (s) return s;
     xd = L->x_stage;
   }
-  if (L->cfg.precision == LCAE_FP32) return launch_nhwc_to_hwcn_f32(L, xd, L->xt32);
-  return launch_nhwc_to_hwcn_bf16(L, xd, L->xt16);
+  lcae_status s = (L->cfg.precision == LCAE_FP32) ? launch_nhwc_to_hwcn_f32(L, xd, L->xt32)
+                                                  : launch_nhwc_to_hwcn_bf16(L, xd, L->xt16);
+  if (s) return s;
+  if (L->x_consumed) LCAE_CK(cudaEventRecord(L->x_consumed, L->st));   // x_pf may be refilled after this
+  return LCAE_OK;
 }
 
 static lcae_status read_loss(lcae_layer *L, double *loss) {
@@ -132,6 +139,10 @@ lcae_status lcae_destroy(lcae_layer *L) {
                   (void *)L->rowsq})
     if (p) cudaFree(p);
   if (L->loss_host) cudaFreeHost(L->loss_host);
+  if (L->x_pf) cudaFree(L->x_pf);
+  if (L->copy_st) cudaStreamDestroy(L->copy_st);
+  if (L->pf_done) cudaEventDestroy(L->pf_done);
+  if (L->x_consumed) cudaEventDestroy(L->x_consumed);
   if (L->prof_ev) {
     for (int i = 0; i < 2 * 4096; ++i) cudaEventDestroy(L->prof_ev[i]);
     delete[] L->prof_ev;
@@ -302,6 +313,26 @@ static lcae_status run(lcae_layer *L, const float *x, bool update, float *dx, fl
 
 lcae_status lcae_forward(lcae_layer *L, const float *x, float *pooled, double *loss) {
   return run(L, x, false, nullptr, pooled, loss);
+}
+
+lcae_status lcae_prefetch_input(lcae_layer *L, const float *x_host) {
+  if (!L || !x_host) { set_error("NULL argument"); return LCAE_ERR_ARG; }
+  if (is_device_ptr(x_host)) return LCAE_OK;   // nothing to copy
+  const Geo &g = L->geo;
+  const size_t bytes = (size_t)g.m * g.H * g.W * g.C * 4;
+  if (!L->x_pf) {   // first use: the buffer, a copy stream and two events
+    LCAE_CK(cudaMalloc(&L->x_pf, bytes));
+    LCAE_CK(cudaStreamCreateWithFlags(&L->copy_st, cudaStreamNonBlocking));
+    LCAE_CK(cudaEventCreateWithFlags(&L->pf_done, cudaEventDisableTiming));
+    LCAE_CK(cudaEventCreateWithFlags(&L->x_consumed, cudaEventDisableTiming));
+    LCAE_CK(cudaEventRecord(L->x_consumed, L->st));
+  }
+  // the previous prefetched batch must have been converted before x_pf is overwritten
+  LCAE_CK(cudaStreamWaitEvent(L->copy_st, L->x_consumed, 0));
+  LCAE_CK(cudaMemcpyAsync(L->x_pf, x_host, bytes, cudaMemcpyHostToDevice, L->copy_st));
+  LCAE_CK(cudaEventRecord(L->pf_done, L->copy_st));
+  L->pf_host = x_host;
+  return LCAE_OK;
 }
 
 lcae_status lcae_encode(lcae_layer *L, const float *x, float *pooled, double *j_sparse) {

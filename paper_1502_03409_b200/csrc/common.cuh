@@ -68,6 +68,11 @@ struct lcae_layer {
   int wp = 0;                                          // row pitch (floats) of W~, vW, gW
   // inputs / outputs
   float *x_stage = nullptr;      // NHWC f32 staging for host inputs
+  // input prefetch (lcae_prefetch_input): host batch copied on its own stream into x_pf, overlapping a step
+  float *x_pf = nullptr;
+  const void *pf_host = nullptr;   // host pointer whose copy is in flight / landed in x_pf
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t pf_done = nullptr, x_consumed = nullptr;
   float *xt32 = nullptr;         // HWCN f32 (fp32 mode)
   __nv_bfloat16 *xt16 = nullptr; // HWCN bf16 (bf16 mode)
   float *dxt = nullptr;          // HWCN f32 dX accumulator

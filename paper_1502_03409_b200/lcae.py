@@ -53,6 +53,7 @@ def _load():
         "lcae_forward": (C.c_int, [P, P, P, C.POINTER(C.c_double)]),
         "lcae_step": (C.c_int, [P, P, P, C.POINTER(C.c_double)]),
         "lcae_encode": (C.c_int, [P, P, P, C.POINTER(C.c_double)]),
+        "lcae_prefetch_input": (C.c_int, [P, P]),
         "lcae_topk_init": (C.c_int, [P, P, C.c_int64, C.c_int32, P]),
         "lcae_lcn": (C.c_int, [P, P, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, P]),
         "lcae_topk_update": (C.c_int, [P, C.c_int64, C.c_int64, C.c_int32, C.c_int64, P, P, P]),
@@ -85,7 +86,7 @@ lib = _load()
 # Every symbol include/lcae.h declares (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("lcae_config_default", "lcae_geometry", "lcae_create", "lcae_destroy", "lcae_set_params",
                "lcae_get_params", "lcae_get_grads", "lcae_forward", "lcae_encode", "lcae_step", "lcae_last_loss",
-               "lcae_topk_init", "lcae_topk_update", "lcae_lcn",
+               "lcae_topk_init", "lcae_topk_update", "lcae_lcn", "lcae_prefetch_input",
                "lcae_dx_device", "lcae_counters", "lcae_region_add", "lcae_last_launch_count",
                "lcae_profile", "lcae_profile_read",
                "lcae_last_error", "lcae_version")
@@ -176,6 +177,10 @@ class Layer:
         loss = C.c_double(0.0)
         check(lib.lcae_forward(self.h, _ptr(x), _ptr(pooled), C.byref(loss) if want_loss else None))
         return loss.value if want_loss else None
+
+    def prefetch_input(self, x_host):
+        """Overlap the host->device copy of the next batch with the current step (lcae_prefetch_input)."""
+        check(lib.lcae_prefetch_input(self.h, _ptr(x_host)))
 
     def encode(self, x, pooled, want_loss=True):
         """Inference: encode + L2 pooling only (lcae_encode); returns J_sparse if want_loss."""
