@@ -843,10 +843,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
                   const float4 vv = *reinterpret_cast<const float4 *>(P.vW + (wp_ - P.W));
                   vo[0] = vv.x; vo[1] = vv.y; vo[2] = vv.z; vo[3] = vv.w;
                 }
+                // the accumulator holds sigma_r dJ/dW: dJ/dW = acc / sigma_r; W~' = sigma_r W~ - lr dJ/dW
+                const float cr = nlr * isgr[i];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                  d[e] = (fullc || cc0 + e < n) ? d0[e] * isgr[i] : 0.f;   // accumulator holds sigma_r * dJ/dW
-                  float upd = nlr * d[e];
+                  const float acc = (fullc || cc0 + e < n) ? d0[e] : 0.f;
+                  d[e] = acc;
+                  float upd = cr * acc;
                   if (has_v) { upd = fmaf(P.mu, vo[e], upd); vo[e] = upd; }
                   wn[e] = fmaf(sgr[i], wo4[e], upd);
                   rsq4[i] = fmaf(wn[e], wn[e], rsq4[i]);
@@ -856,7 +859,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
                   ptx::st_u2_ef(P.Wb + ((int64_t)f * KP + r) * P.n_al + cc0,
                                 make_uint2(ptx::pack_bf16x2(wn[0], wn[1]), ptx::pack_bf16x2(wn[2], wn[3])), pol_ef);
                 if (has_v) *reinterpret_cast<float4 *>(P.vW + (wp_ - P.W)) = make_float4(vo[0], vo[1], vo[2], vo[3]);
-                if (keep) *reinterpret_cast<float4 *>(P.gW + (wp_ - P.W)) = make_float4(d[0], d[1], d[2], d[3]);
+                if (keep) {
+                  const float is = isgr[i];
+                  *reinterpret_cast<float4 *>(P.gW + (wp_ - P.W)) = make_float4(d[0] * is, d[1] * is, d[2] * is, d[3] * is);
+                }
               }
             }
           }
