@@ -736,16 +736,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           TWAIT(18, ptx::mbar_wait(&S.p2_full[pb], (u2 / NB2) & 1));
           ptx::tc_fence_after();
           TMARK(35);
+          const int swr = (lane >> 1) & 3;                     // swizzle of this lane's row (row = lane)
+          float *stg = &S.stg[ew][0][0];                       // [32 rows][16] fp32, 16-byte chunks swizzled
+          const float *rcv = &S.recv[half][qd * 32][0];        // same layout, written by the peer
           // dx = alpha W^T D - delta (both halves accumulated in TMEM), overlap-added into the image gradient with
           // 16-byte reductions: 4x4 lane transposes give each lane 4 consecutive samples of one column.
-          {
+          auto dx_reduce = [&](const float (&xv)[32]) {
             const int r4 = lane & 3;
             const bool o1 = r4 & 1, o2 = r4 & 2;
             const bool full = (j + 1) * NT <= n;   // all but the ragged last tile
-            float xv[32];
-            ptx::tmem_ld16(tl + base + hc, xv);
-            ptx::tmem_ld16(tl + base + hc + 16, xv + 16);
-            ptx::tmem_ld_wait();
 #pragma unroll
             for (int blk = 0; blk < 8; ++blk) {
               float a0 = xv[4 * blk], a1 = xv[4 * blk + 1], a2 = xv[4 * blk + 2], a3 = xv[4 * blk + 3];
@@ -757,15 +756,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               if (o2) { a0 = t0; a1 = t1; } else { a2 = t0; a3 = t1; }
               const int nn = j * NT + hc + 4 * blk + r4;
               ptx::red_v4_if(dxcol + (uint32_t)S.off[nn] * (uint32_t)mp, a0, a1, a2, a3,
-                        (full || nn < n) && grp_ok && do_red);
+                             (full || nn < n) && grp_ok && do_red);
             }
-          }
-          TMARK(36);
+          };
           // dW_j (lanes = filter rows, this warp's 32 columns). CTA c owns the 16-column chunk [16c, 16c+16) of
           // each half; the batch slices of that chunk are summed over the cluster (DSMEM), then the projected SGD
-          // runs in a coalesced layout: the summed chunk is transposed through this warp's 2 KB staging slice
-          // (its rows of `recv`) so that lane l updates rows 8i + l/4, columns 4(l%4)..+3 (64-byte row runs).
-          float4 wv[4 * NCH];   // owned W~ runs, coalesced layout (issued before the dW wait)
+          // runs in a coalesced layout: the own chunk is transposed through this warp's 2 KB staging slice and
+          // the peer's is read from the receive slice, so that lane l updates rows 8i + l/4, columns 4(l%4)..+3.
+          float4 wv[4 * NCH];   // owned W~ runs, coalesced layout (issued before the dW read)
 #pragma unroll
           for (int h = 0; h < NCH; ++h) {
             const int cc0 = j * NT + hc + oc + 16 * h + 4 * cq;
@@ -774,45 +772,49 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               wv[4 * h + i] = (rok[i] && cc0 < P.wp) ? ptx::ld_f4_ef(wrp[i] + j * NT + 16 * h, pol_ef)
                                                      : make_float4(0, 0, 0, 0);
           }
-          float dw[32];   // CB = 2: dw[0..15] = the owned chunk, dw[16..31] = the peer's chunk
-          ptx::tmem_ld16(tl + base + 64 + hc + (CB > 1 ? 16 * crank : 0), dw);
-          ptx::tmem_ld16(tl + base + 64 + hc + (CB > 1 ? 16 * (1 - crank) : 16), dw + 16);
-          ptx::tmem_ld_wait();
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&S.p2_empty[pb]);   // TMEM buffer pb fully read by this warp
-          TMARK(40);
-          float *stg = &S.stg[ew][0][0];                       // [32 rows][16] fp32, 16-byte chunks swizzled
-          const float *rcv = &S.recv[half][qd * 32][0];        // same layout, written by the peer
-          const int swr = (lane >> 1) & 3;                     // swizzle of this lane's row (row = lane)
-          if (CB > 1) {
-            const uint32_t peer = crank ^ 1u;
-            // arm this tile's receive phase: 8 warps x 32 rows x 16 floats arrive from the peer via st.async
-            if (etid == 0) ptx::mbar_arrive_expect_tx(&S.recv_full, 2 * 128 * 16 * 4);
-            TWAIT(22, ptx::mbar_wait(&S.peer_free, (u2 & 1) ^ 1));
-            const uint32_t rdst = peer_recv, rbar = peer_recv_full;
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-              ptx::st_async_v4(rdst + 16 * (t ^ swr),
-                               make_float4(dw[16 + 4 * t], dw[17 + 4 * t], dw[18 + 4 * t], dw[19 + 4 * t]), rbar);
-          }
-          TMARK(41);
           float4 dq[4 * NCH];   // summed dW chunk(s), coalesced layout
+          if constexpr (CB > 1) {
+            // the dW half the peer owns goes out first and the own half is staged, so that the exchange is in
+            // flight while this warp reduces dX
+            {
+              float dw[32];   // dw[0..15] = the owned chunk, dw[16..31] = the peer's chunk
+              ptx::tmem_ld16(tl + base + 64 + hc + 16 * crank, dw);
+              ptx::tmem_ld16(tl + base + 64 + hc + 16 * (1 - crank), dw + 16);
+              ptx::tmem_ld_wait();
+              // arm this tile's receive phase: 8 warps x 32 rows x 16 floats arrive from the peer via st.async
+              if (etid == 0) ptx::mbar_arrive_expect_tx(&S.recv_full, 2 * 128 * 16 * 4);
+              TWAIT(22, ptx::mbar_wait(&S.peer_free, (u2 & 1) ^ 1));
 #pragma unroll
-          for (int h = 0; h < NCH; ++h) {
+              for (int t = 0; t < 4; ++t)
+                ptx::st_async_v4(peer_recv + 16 * (t ^ swr),
+                                 make_float4(dw[16 + 4 * t], dw[17 + 4 * t], dw[18 + 4 * t], dw[19 + 4 * t]),
+                                 peer_recv_full);
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
-              *reinterpret_cast<float4 *>(stg + lane * 16 + 4 * (t ^ swr)) =
-                  make_float4(dw[16 * h + 4 * t], dw[16 * h + 4 * t + 1], dw[16 * h + 4 * t + 2], dw[16 * h + 4 * t + 3]);
+              for (int t = 0; t < 4; ++t)
+                *reinterpret_cast<float4 *>(stg + lane * 16 + 4 * (t ^ swr)) =
+                    make_float4(dw[4 * t], dw[4 * t + 1], dw[4 * t + 2], dw[4 * t + 3]);
+            }
+            TMARK(40);
+            {
+              float xv[32];
+              ptx::tmem_ld16(tl + base + hc, xv);
+              ptx::tmem_ld16(tl + base + hc + 16, xv + 16);
+              ptx::tmem_ld_wait();
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive(&S.p2_empty[pb]);   // TMEM buffer pb fully read by this warp
+              dx_reduce(xv);
+            }
+            TMARK(36);
             __syncwarp();
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const int r = 8 * i + rr, o = r * 16 + 4 * (cq ^ ((r >> 1) & 3));
-              dq[4 * h + i] = *reinterpret_cast<const float4 *>(stg + o);
+              dq[i] = *reinterpret_cast<const float4 *>(stg + o);
             }
             __syncwarp();
-          }
-          if (CB > 1) {   // + the peer's batch slice, read straight from the receive slice in the same layout
+            TMARK(41);
+            // + the peer's batch slice, read straight from the receive slice in the same layout
             TWAIT(22, ptx::mbar_wait(&S.recv_full, u2 & 1));
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -823,6 +825,39 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             __syncwarp();
             if (lane == 0)   // receive slice read: the peer may send the next tile (reads only; relaxed suffices)
               ptx::mbar_arrive_remote_relaxed(peer_free_bar);
+          } else {
+            {
+              float xv[32];
+              ptx::tmem_ld16(tl + base + hc, xv);
+              ptx::tmem_ld16(tl + base + hc + 16, xv + 16);
+              ptx::tmem_ld_wait();
+              dx_reduce(xv);
+            }
+            TMARK(36);
+            float dw[32];
+            ptx::tmem_ld16(tl + base + 64 + hc, dw);
+            ptx::tmem_ld16(tl + base + 64 + hc + 16, dw + 16);
+            ptx::tmem_ld_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&S.p2_empty[pb]);   // TMEM buffer pb fully read by this warp
+            TMARK(40);
+            TMARK(41);
+#pragma unroll
+            for (int h = 0; h < NCH; ++h) {
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+                *reinterpret_cast<float4 *>(stg + lane * 16 + 4 * (t ^ swr)) =
+                    make_float4(dw[16 * h + 4 * t], dw[16 * h + 4 * t + 1], dw[16 * h + 4 * t + 2],
+                                dw[16 * h + 4 * t + 3]);
+              __syncwarp();
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int r = 8 * i + rr, o = r * 16 + 4 * (cq ^ ((r >> 1) & 3));
+                dq[4 * h + i] = *reinterpret_cast<const float4 *>(stg + o);
+              }
+              __syncwarp();
+            }
           }
           TMARK(42);
           if (do_sgd) {
