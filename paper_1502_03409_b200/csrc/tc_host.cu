@@ -211,8 +211,10 @@ lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_on
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void (*kern)(tc::Params) = nullptr;
-#define LCAE_PICK(GPV)                                                        \
-  if (g.g == GPV) kern = s->CB == 1 ? tc::step_kernel<GPV, 1> : tc::step_kernel<GPV, 2>;
+#define LCAE_PICK(GPV)                                                                                  \
+  if (g.g == GPV)                                                                                       \
+    kern = s->trace_on ? (s->CB == 1 ? tc::step_kernel<GPV, 1, true> : tc::step_kernel<GPV, 2, true>)     \
+                       : (s->CB == 1 ? tc::step_kernel<GPV, 1, false> : tc::step_kernel<GPV, 2, false>);
   LCAE_PICK(1) LCAE_PICK(2) LCAE_PICK(4) LCAE_PICK(8) LCAE_PICK(16) LCAE_PICK(32)
 #undef LCAE_PICK
   if (!kern) { set_error("unsupported pool group"); return LCAE_ERR_CONFIG; }

@@ -160,7 +160,7 @@ __device__ __forceinline__ float residual32(float (&rv)[32], int c0, int n, cons
   return jr;
 }
 
-template <int GP, int CBT>
+template <int GP, int CBT, bool TR>   // TR: wait / section tracing compiled in (lcae_dev_trace builds only)
 __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant__ Params P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the SW128 tiles by pointer arithmetic on the shared array (keeps the shared
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
   const bool step = P.mode == 1;
   const bool enc = P.mode == 2;   // encode-only inference (pass 0 + pooling)
   // trace: lane 0 of the producers / MMA warp and of epilogue warp 2 record their barrier-wait cycles
-  const bool trec = P.trace != nullptr && lane == 0 && (warp <= 2 || warp == XWARP);
+  const bool trec = TR && P.trace != nullptr && lane == 0 && (warp <= 2 || warp == XWARP);
   const long long t_start = clock64();
 #define TWAIT(IDX, ...)                                                                          \
   do {                                                                                           \
