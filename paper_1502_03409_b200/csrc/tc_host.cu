@@ -211,10 +211,14 @@ lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_on
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void (*kern)(tc::Params) = nullptr;
-#define LCAE_PICK(GPV)                                                                                  \
-  if (g.g == GPV)                                                                                       \
-    kern = s->trace_on ? (s->CB == 1 ? tc::step_kernel<GPV, 1, true> : tc::step_kernel<GPV, 2, true>)     \
-                       : (s->CB == 1 ? tc::step_kernel<GPV, 1, false> : tc::step_kernel<GPV, 2, false>);
+  // variant: lean (plain SGD, no kept gradients, no debug flags), full, or traced (full + wait trace)
+  const int fl = s->trace_on ? 3 : ((L->vW || L->cfg.keep_grads || P.dbg) ? 2 : 0);
+#define LCAE_PICK(GPV)                                                                                   \
+  if (g.g == GPV) {                                                                                      \
+    if (fl == 0) kern = s->CB == 1 ? tc::step_kernel<GPV, 1, 0> : tc::step_kernel<GPV, 2, 0>;             \
+    else if (fl == 2) kern = s->CB == 1 ? tc::step_kernel<GPV, 1, 2> : tc::step_kernel<GPV, 2, 2>;        \
+    else kern = s->CB == 1 ? tc::step_kernel<GPV, 1, 3> : tc::step_kernel<GPV, 2, 3>;                     \
+  }
   LCAE_PICK(1) LCAE_PICK(2) LCAE_PICK(4) LCAE_PICK(8) LCAE_PICK(16) LCAE_PICK(32)
 #undef LCAE_PICK
   if (!kern) { set_error("unsupported pool group"); return LCAE_ERR_CONFIG; }

@@ -160,7 +160,9 @@ __device__ __forceinline__ float residual32(float (&rv)[32], int c0, int n, cons
   return jr;
 }
 
-template <int GP, int CBT, bool TR>   // TR: wait / section tracing compiled in (lcae_dev_trace builds only)
+// FL bit 0: wait / section tracing compiled in (lcae_dev_trace); bit 1: the full epilogue (momentum velocity,
+// kept gradients, debug flags). The lean variant (FL = 0) is the common training step.
+template <int GP, int CBT, int FL>
 __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant__ Params P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the SW128 tiles by pointer arithmetic on the shared array (keeps the shared
@@ -177,6 +179,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
   const bool step = P.mode == 1;
   const bool enc = P.mode == 2;   // encode-only inference (pass 0 + pooling)
   // trace: lane 0 of the producers / MMA warp and of epilogue warp 2 record their barrier-wait cycles
+  constexpr bool TR = (FL & 1) != 0, FULL = (FL & 2) != 0;
   const bool trec = TR && P.trace != nullptr && lane == 0 && (warp <= 2 || warp == XWARP);
   const long long t_start = clock64();
 #define TWAIT(IDX, ...)                                                                          \
@@ -716,7 +719,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         const int rr = lane >> 2, cq = lane & 3;
         const int64_t wrow0 = (int64_t)f * k + qd * 32 + rr;   // W~ master row of i = 0
         // per-field invariants of this thread's E2 work, hoisted out of the tile loop
-        const bool do_red = !(P.dbg & 1), do_sgd = !(P.dbg & 2), has_v = P.vW != nullptr, keep = P.keep_grads != 0;
+        const bool do_red = !FULL || !(P.dbg & 1), do_sgd = !FULL || !(P.dbg & 2);
+        const bool has_v = FULL && P.vW != nullptr, keep = FULL && P.keep_grads != 0;
         float *const dxcol = P.dxt + pixbase * mp + (s0 + qd * 32 + (lane & ~3));   // dX band of this lane group
         const bool grp_ok = s0 + qd * 32 + (lane & ~3) < mp;
         const float *wrp[4];

@@ -99,3 +99,16 @@ def test_bf16_parity(name):
     errs = _compare(shape, 1, out, o, W.astype(np.float64), a.astype(np.float64), b.astype(np.float64))
     print(name, {k_: f"{v:.1e}" for k_, v in errs.items()})
     assert out["steps"] == 1 and out["reinit"] == 0
+
+
+@pytest.mark.parametrize("name", ["c1", "ragged", "cluster2", "c3tiny"])
+def test_bf16_lean_variant_parity(name):
+    """The production (lean) step kernel variant -- no kept gradients, no velocity, no debug flags -- against the
+    oracle: loss and the W / alpha / b updates (the keep_grads tests above run the full variant)."""
+    shape = SHAPES_BF16[name]
+    W, a, b = make_params(shape, seed=0)
+    X = make_images(shape, seed=1)
+    b = (0.05 * np.random.default_rng(3).standard_normal(b.shape)).astype(np.float32)
+    out = gpu_step(shape, 1, W, a, b, X, keep_grads=False, forward_first=False)
+    o = oracle_step(shape, W, a, b, X)
+    _compare(shape, 1, out, o, W, a, b)
