@@ -568,6 +568,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         for (int t = 0; t < 32; ++t) u[t] *= S.sig[cc * 32 + t];
         constexpr int NGC = 32 / GP;   // pooling groups per 32-filter chunk
         float pv[NGC];
+        float jsc = 0.f;   // this chunk's sum of s_G (fp32 over <= 32 terms, then into the fp64 total)
 #pragma unroll
         for (int G0 = 0; G0 < 32; G0 += GP) {
           float ss = 0.f;
@@ -577,8 +578,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           const float v = P.eps + ss;
           const float sG = v > 0.f ? v * rsqrtf(v) : 0.f;   // sqrt(eps + sum_G h^2)
           pv[G0 / GP] = sG;
-          if (G < ng && svalid) js += (double)sG;
+          if (G < ng) jsc += sG;
         }
+        if (svalid) js += (double)jsc;
         if (P.want_pooled) {   // p [m][gr][gc][ng] (forward / encode only: recv + stg are idle then)
           const int G0c = cc * NGC;   // first group of the chunk
           if constexpr (NGC >= 4) {
