@@ -211,13 +211,15 @@ lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_on
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void (*kern)(tc::Params) = nullptr;
-  // variant: lean (plain SGD, no kept gradients, no debug flags), full, or traced (full + wait trace)
-  const int fl = s->trace_on ? 3 : ((L->vW || L->cfg.keep_grads || P.dbg) ? 2 : 0);
+  // variant: training step lean (plain SGD, no kept gradients, no debug flags), full, or traced (full + wait
+  // trace); forward / encode run the generic variant
+  const int fl = !update ? 6 : s->trace_on ? 3 : ((L->vW || L->cfg.keep_grads || P.dbg) ? 2 : 0);
 #define LCAE_PICK(GPV)                                                                                   \
   if (g.g == GPV) {                                                                                      \
     if (fl == 0) kern = s->CB == 1 ? tc::step_kernel<GPV, 1, 0> : tc::step_kernel<GPV, 2, 0>;             \
     else if (fl == 2) kern = s->CB == 1 ? tc::step_kernel<GPV, 1, 2> : tc::step_kernel<GPV, 2, 2>;        \
-    else kern = s->CB == 1 ? tc::step_kernel<GPV, 1, 3> : tc::step_kernel<GPV, 2, 3>;                     \
+    else if (fl == 3) kern = s->CB == 1 ? tc::step_kernel<GPV, 1, 3> : tc::step_kernel<GPV, 2, 3>;        \
+    else kern = s->CB == 1 ? tc::step_kernel<GPV, 1, 6> : tc::step_kernel<GPV, 2, 6>;                     \
   }
   LCAE_PICK(1) LCAE_PICK(2) LCAE_PICK(4) LCAE_PICK(8) LCAE_PICK(16) LCAE_PICK(32)
 #undef LCAE_PICK

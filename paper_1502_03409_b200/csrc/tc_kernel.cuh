@@ -161,7 +161,8 @@ __device__ __forceinline__ float residual32(float (&rv)[32], int c0, int n, cons
 }
 
 // FL bit 0: wait / section tracing compiled in (lcae_dev_trace); bit 1: the full epilogue (momentum velocity,
-// kept gradients, debug flags). The lean variant (FL = 0) is the common training step.
+// kept gradients, debug flags); bit 2: generic mode (forward / encode). The lean variant (FL = 0) is the common
+// training step.
 template <int GP, int CBT, int FL>
 __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant__ Params P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -176,10 +177,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
   const int cid = blockIdx.x / CB, ncl = gridDim.x / CB;
   const int s0 = (int)crank * MC;   // first sample of this CTA
   const int T = P.T, n = g.n, k = g.k, m = g.m, mp = P.mp;
-  const bool step = P.mode == 1;
-  const bool enc = P.mode == 2;   // encode-only inference (pass 0 + pooling)
+  // FL bit 2: generic variant (forward / encode / step chosen at run time, pooled output); otherwise the
+  // kernel is the training step and the forward-only paths are compiled out
+  constexpr bool TR = (FL & 1) != 0, FULL = (FL & 2) != 0, GEN = (FL & 4) != 0;
+  const bool step = GEN ? P.mode == 1 : true;
+  const bool enc = GEN && P.mode == 2;   // encode-only inference (pass 0 + pooling)
+  const bool want_pooled = GEN && P.want_pooled;
   // trace: lane 0 of the producers / MMA warp and of epilogue warp 2 record their barrier-wait cycles
-  constexpr bool TR = (FL & 1) != 0, FULL = (FL & 2) != 0;
   const bool trec = TR && P.trace != nullptr && lane == 0 && (warp <= 2 || warp == XWARP);
   const long long t_start = clock64();
 #define TWAIT(IDX, ...)                                                                          \
@@ -581,7 +585,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           if (G < ng) jsc += sG;
         }
         if (svalid) js += (double)jsc;
-        if (P.want_pooled) {   // p [m][gr][gc][ng] (forward / encode only: recv + stg are idle then)
+        if (want_pooled) {   // p [m][gr][gc][ng] (forward / encode only: recv + stg are idle then)
           const int G0c = cc * NGC;   // first group of the chunk
           if constexpr (NGC >= 4) {
             // coalesced: the warp's 32 samples x NGC groups are transposed through 4 KB of staging so that
