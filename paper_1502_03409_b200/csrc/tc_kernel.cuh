@@ -782,6 +782,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               wv[4 * h + i] = (rok[i] && cc0 < P.wp) ? ptx::ld_f4_ef(wrp[i] + j * NT + 16 * h, pol_ef)
                                                      : make_float4(0, 0, 0, 0);
           }
+          float4 vvp[FULL ? 4 * NCH : 1];   // momentum velocity runs, issued with the W~ runs (full variant)
+          if constexpr (FULL) {
+#pragma unroll
+            for (int h = 0; h < NCH; ++h) {
+              const int cc0 = j * NT + hc + oc + 16 * h + 4 * cq;
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                vvp[4 * h + i] = (has_v && rok[i] && cc0 < P.wp)
+                                     ? ptx::ld_f4_ef(P.vW + (wrp[i] - P.W) + j * NT + 16 * h, pol_ef)
+                                     : make_float4(0, 0, 0, 0);
+            }
+          }
           float4 dq[4 * NCH];   // summed dW chunk(s), coalesced layout
           if constexpr (CB > 1) {
             // the dW half the peer owns goes out first and the own half is staged, so that the exchange is in
@@ -884,8 +896,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
                 const float d0[4] = {dq[4 * h + i].x, dq[4 * h + i].y, dq[4 * h + i].z, dq[4 * h + i].w};
                 const float wo4[4] = {wv[4 * h + i].x, wv[4 * h + i].y, wv[4 * h + i].z, wv[4 * h + i].w};
                 float d[4], wn[4], vo[4] = {0.f, 0.f, 0.f, 0.f};
-                if (has_v) {
-                  const float4 vv = *reinterpret_cast<const float4 *>(P.vW + (wp_ - P.W));
+                if constexpr (FULL) {
+                  const float4 vv = vvp[4 * h + i];
                   vo[0] = vv.x; vo[1] = vv.y; vo[2] = vv.z; vo[3] = vv.w;
                 }
                 // the accumulator holds sigma_r dJ/dW: dJ/dW = acc / sigma_r; W~' = sigma_r W~ - lr dJ/dW
