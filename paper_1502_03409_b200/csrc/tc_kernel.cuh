@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           for (int t = 0; t < GP; ++t) { float h = a * u[G0 + t]; ss = fmaf(h, h, ss); }
           const int G = (cc * 32 + G0) / GP;
           const float v = P.eps + ss;
-          const float sG = v > 0.f ? v * rsqrtf(v) : 0.f;   // sqrt(eps + sum_G h^2)
+          const float sG = v * rsqrtf(fmaxf(v, 1.17549435e-38f));   // sqrt(eps + sum_G h^2); 0 at v = 0
           pv[G0 / GP] = sG;
           if (G < ng) jsc += sG;
         }
@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
 #pragma unroll
             for (int t = 0; t < GP; ++t) { float h = a * u[G0 + t]; ss = fmaf(h, h, ss); }
             const float v = P.eps + ss;
-            const float inv = v > 0.f ? P.lam * rsqrtf(v) : 0.f;   // lambda / s_G
+            const float inv = P.lam * rsqrtf(fmaxf(v, 1.17549435e-38f));   // lambda / s_G (v = 0 only with h = 0: R12)
 #pragma unroll
             for (int t = 0; t < GP; ++t) {
               const int col = cc * 32 + G0 + t;
