@@ -28,6 +28,67 @@ __global__ void nhwc_to_hwcn(const float *__restrict__ x, T *__restrict__ xt, in
   }
 }
 
+// Vectorised 64 x 64 variants (16-byte global accesses on both sides; used when P % 4 == 0):
+// NHWC f32 [m][P] -> HWCN bf16 [P][mp] (sample rows in [m, mp) written as zeros).
+__global__ void __launch_bounds__(256) nhwc_to_hwcn_bf16_v(const float *__restrict__ x, __nv_bfloat16 *__restrict__ xt,
+                                                           int m, int mp, int64_t P) {
+  __shared__ float tile[64][65];   // [sample][pixel-feature]
+  const int64_t p0 = (int64_t)blockIdx.x * 64;
+  const int i0 = blockIdx.y * 64, t = threadIdx.x;
+  for (int r = t / 16; r < 64; r += 16) {   // 16 lanes x float4 = 64 pixel-features of one sample
+    const int i = i0 + r, c4 = t % 16;
+    const int64_t p = p0 + 4 * c4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < m && p < P) v = __ldg(reinterpret_cast<const float4 *>(x + (int64_t)i * P + p));
+    tile[r][4 * c4] = v.x;
+    tile[r][4 * c4 + 1] = v.y;
+    tile[r][4 * c4 + 2] = v.z;
+    tile[r][4 * c4 + 3] = v.w;
+  }
+  __syncthreads();
+  for (int q = t / 8; q < 64; q += 32) {   // 8 lanes x 8 bf16 = 64 samples of one pixel-feature
+    const int g8 = t % 8, i = i0 + 8 * g8;
+    const int64_t p = p0 + q;
+    if (p >= P || i >= mp) continue;
+    uint4 o;
+    uint32_t *w = reinterpret_cast<uint32_t *>(&o);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float a = i + 2 * e < m ? tile[8 * g8 + 2 * e][q] : 0.f;
+      const float b = i + 2 * e + 1 < m ? tile[8 * g8 + 2 * e + 1][q] : 0.f;
+      __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+      w[e] = *reinterpret_cast<uint32_t *>(&h);
+    }
+    *reinterpret_cast<uint4 *>(xt + p * mp + i) = o;
+  }
+}
+
+// HWCN f32 [P][mp] -> NHWC f32 [m][P]
+__global__ void __launch_bounds__(256) hwcn_to_nhwc_v(const float *__restrict__ xt, float *__restrict__ x, int m, int mp,
+                                                      int64_t P) {
+  __shared__ float tile[64][65];   // [pixel-feature][sample]
+  const int64_t p0 = (int64_t)blockIdx.x * 64;
+  const int i0 = blockIdx.y * 64, t = threadIdx.x;
+  for (int r = t / 16; r < 64; r += 16) {   // 16 lanes x float4 = 64 samples of one pixel-feature
+    const int64_t p = p0 + r;
+    const int c4 = t % 16, i = i0 + 4 * c4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (p < P && i < mp) v = __ldg(reinterpret_cast<const float4 *>(xt + p * mp + i));
+    tile[r][4 * c4] = v.x;
+    tile[r][4 * c4 + 1] = v.y;
+    tile[r][4 * c4 + 2] = v.z;
+    tile[r][4 * c4 + 3] = v.w;
+  }
+  __syncthreads();
+  for (int q = t / 16; q < 64; q += 16) {   // 16 lanes x float4 = 64 pixel-features of one sample
+    const int i = i0 + q, c4 = t % 16;
+    const int64_t p = p0 + 4 * c4;
+    if (i >= m || p >= P) continue;
+    *reinterpret_cast<float4 *>(x + (int64_t)i * P + p) =
+        make_float4(tile[4 * c4][q], tile[4 * c4 + 1][q], tile[4 * c4 + 2][q], tile[4 * c4 + 3][q]);
+  }
+}
+
 __global__ void hwcn_to_nhwc(const float *__restrict__ xt, float *__restrict__ x, int m, int mp, int64_t P) {
   __shared__ float tile[32][33];
   const int64_t p0 = (int64_t)blockIdx.x * 32;
@@ -136,6 +197,12 @@ lcae_status launch_nhwc_to_hwcn_f32(lcae_layer *L, const float *x, float *xt) {
 lcae_status launch_nhwc_to_hwcn_bf16(lcae_layer *L, const float *x, __nv_bfloat16 *xt) {
   const Geo &g = L->geo;
   int64_t P = (int64_t)g.H * g.W * g.C;
+  if (P % 4 == 0 && L->mp % 8 == 0 && ((uintptr_t)x & 15) == 0) {
+    dim3 gv((unsigned)((P + 63) / 64), (unsigned)cdiv(g.m, 64));
+    nhwc_to_hwcn_bf16_v<<<gv, 256, 0, L->st>>>(x, xt, g.m, L->mp, P);
+    LCAE_CK_LAUNCH(L);
+    return LCAE_OK;
+  }
   dim3 grid((unsigned)cdiv((int)P, 32), cdiv(g.m, 32));
   nhwc_to_hwcn<__nv_bfloat16><<<grid, dim3(32, 8), 0, L->st>>>(x, xt, g.m, L->mp, P);
   LCAE_CK_LAUNCH(L);
@@ -145,6 +212,12 @@ lcae_status launch_nhwc_to_hwcn_bf16(lcae_layer *L, const float *x, __nv_bfloat1
 lcae_status launch_hwcn_to_nhwc_f32(lcae_layer *L, const float *xt, float *x) {
   const Geo &g = L->geo;
   int64_t P = (int64_t)g.H * g.W * g.C;
+  if (P % 4 == 0 && L->mp % 4 == 0 && ((uintptr_t)x & 15) == 0) {
+    dim3 gv((unsigned)((P + 63) / 64), (unsigned)cdiv(g.m, 64));
+    hwcn_to_nhwc_v<<<gv, 256, 0, L->st>>>(xt, x, g.m, L->mp, P);
+    LCAE_CK_LAUNCH(L);
+    return LCAE_OK;
+  }
   dim3 grid((unsigned)cdiv((int)P, 32), cdiv(g.m, 32));
   hwcn_to_nhwc<<<grid, dim3(32, 8), 0, L->st>>>(xt, x, g.m, L->mp, P);
   LCAE_CK_LAUNCH(L);
