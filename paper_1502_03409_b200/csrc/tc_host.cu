@@ -1,5 +1,6 @@
 // tc_host.cu — finalize kernel (alpha/b update, row scales, degenerate rows) and host launch code of the bf16
 // tcgen05 step (kernel in tc_kernel.cuh).
+#include <cfloat>
 #include "tc_kernel.cuh"
 #include "tma_host.cuh"
 
@@ -42,7 +43,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(Geo g, int CB, int n_al, 
   for (int r = threadIdx.x; r < k; r += blockDim.x) {
     float rs = 0.f;
     for (int c = 0; c < 2 * CB; ++c) rs += rowsq_part[((int64_t)f * 2 * CB + c) * KP + r];   // [F][CB][2 halves][KP]
-    if (!(rs > 0.f)) {
+    if (!(rs >= FLT_MIN)) {   // R13 in fp32: squared row norm below the smallest normal float
       int slot = atomicAdd(&nbad, 1);
       bad[slot] = r;
     } else {
