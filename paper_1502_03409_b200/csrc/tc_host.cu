@@ -30,7 +30,30 @@ __global__ void __launch_bounds__(128) finalize_kernel(Geo g, int CB, int n_al, 
     if (galpha) galpha[f] = da;
     nbad = 0;
   }
-  for (int nn = threadIdx.x; nn < n; nn += blockDim.x) {
+  const bool vec4 = (n & 3) == 0 &&
+                    (((uintptr_t)db_part | (uintptr_t)bvec | (uintptr_t)vb | (uintptr_t)gb) & 15) == 0;
+  if (vec4) {   // same arithmetic as the scalar loop below, four b entries per thread-iteration (16-byte accesses)
+    const int n4 = n >> 2;
+    for (int q = threadIdx.x; q < n4; q += blockDim.x) {
+      float4 db = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c = 0; c < CB; ++c) {
+        const float4 p = reinterpret_cast<const float4 *>(db_part + ((int64_t)f * CB + c) * n)[q];
+        db.x += p.x; db.y += p.y; db.z += p.z; db.w += p.w;
+      }
+      float4 ub = make_float4(-lr * db.x, -lr * db.y, -lr * db.z, -lr * db.w);
+      const int64_t o4 = (int64_t)f * n4 + q;
+      if (vb) {
+        const float4 v = reinterpret_cast<const float4 *>(vb)[o4];
+        ub = make_float4(fmaf(mu, v.x, ub.x), fmaf(mu, v.y, ub.y), fmaf(mu, v.z, ub.z), fmaf(mu, v.w, ub.w));
+        reinterpret_cast<float4 *>(vb)[o4] = ub;
+      }
+      float4 bo = reinterpret_cast<const float4 *>(bvec)[o4];
+      bo.x += ub.x; bo.y += ub.y; bo.z += ub.z; bo.w += ub.w;
+      reinterpret_cast<float4 *>(bvec)[o4] = bo;
+      if (gb) reinterpret_cast<float4 *>(gb)[o4] = db;
+    }
+  }
+  for (int nn = vec4 ? n : threadIdx.x; nn < n; nn += blockDim.x) {
     float db = 0.f;
     for (int c = 0; c < CB; ++c) db += db_part[((int64_t)f * CB + c) * n + nn];
     float ub = -lr * db;
