@@ -30,6 +30,16 @@
  *  - A layer handle is not thread-safe; one handle per host thread.
  *  - The library owns all device memory it allocates; nothing is freed by the caller.
  *
+ * Errors of the data ("non-finite ... numeric error"; SPEC.md:531 exit codes 3/4)
+ *  - The input staging kernel flags any non-finite x element on the device; a loss reduction that yields a
+ *    non-finite J flags that too. Flags are sticky: while one is set, every parameter-updating kernel of
+ *    lcae_step returns without writing (the flagged step itself is skipped when the input was bad; with a
+ *    non-finite loss the step that produced it has already updated its parameters, later steps are skipped).
+ *  - The flag is reported -- LCAE_ERR_DATA for a non-finite input, LCAE_ERR_NUMERIC for a non-finite loss --
+ *    and cleared by the next call that synchronises: a step/forward with loss != NULL, a call with host
+ *    outputs, or lcae_sync. lcae_set_params also clears it. With loss == NULL (the asynchronous hot path)
+ *    nothing is silently written into W after a bad input: the step is skipped on the device.
+ *
  * Layouts (canonical, exchanged with callers and the test oracle)
  *  - image x / dx: NHWC float32 [m][img_h][img_w][img_c].
  *  - W: float32 [F][k][n], n = (ry*rf_w + rx)*img_c + c; alpha: float32 [F]; b: float32 [F][n].
@@ -55,6 +65,7 @@ typedef enum {
   LCAE_ERR_DATA = 3,    /* bad data pointer, shape or non-finite input */
   LCAE_ERR_NUMERIC = 4, /* non-finite loss ("numeric error") */
   LCAE_ERR_CUDA = 5,    /* CUDA runtime / driver failure (message has the CUDA error string) */
+  LCAE_ERR_NCCL = 6,    /* NCCL communicator / transfer failure of a model-parallel layer (lcae_mp_*) */
   LCAE_ERR_ARG = 7      /* NULL handle or NULL required pointer */
 } lcae_status;
 
@@ -150,6 +161,15 @@ lcae_status lcae_prefetch_input(lcae_layer *L, const float *x_host);
  * update. loss (nullable) receives J = J_rec + J_sparse of the pre-update parameters (synchronises).
  * Errors: ARG, DATA, NUMERIC (non-finite loss, parameters already updated), CUDA. */
 lcae_status lcae_step(lcae_layer *L, const float *x, float *dx, double *loss);
+
+/* Wait for the layer's stream and report the sticky data errors (see "Errors of the data" above): LCAE_OK,
+ * LCAE_ERR_DATA (a non-finite input was seen) or LCAE_ERR_NUMERIC (a non-finite loss); clears the flag. */
+lcae_status lcae_sync(lcae_layer *L);
+
+/* Per-field loss of the last step/forward: out[f][0] = J_rec of field f, out[f][1] = J_sparse (lambda sum s_G),
+ * f in this layer's row-major field order; out is host or device memory of 2*F doubles. Synchronises.
+ * (Sampled parity checks at full size compare single fields against the oracle.) Errors: ARG, CUDA. */
+lcae_status lcae_field_losses(lcae_layer *L, double *out);
 
 /* Loss split of the last step/forward: J_rec and J_sparse (host doubles; synchronises). */
 lcae_status lcae_last_loss(lcae_layer *L, double *j_rec, double *j_sparse);

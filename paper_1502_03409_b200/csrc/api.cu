@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -82,12 +83,37 @@ static lcae_status stage_input(lcae_layer *L, const float *x) {
   return LCAE_OK;
 }
 
+// Report (and clear) the sticky device error flags; the stream must be synchronised with flags_host filled.
+static lcae_status flag_status(lcae_layer *L) {
+  const int f0 = L->flags_host[0], f1 = L->flags_host[1];
+  if (!(f0 | f1)) return LCAE_OK;
+  LCAE_CK(cudaMemsetAsync(L->flags_dev, 0, 2 * sizeof(int), L->st));
+  L->flags_host[0] = L->flags_host[1] = 0;
+  if (f0) {
+    set_error("non-finite input value (SPEC.md:95): the flagged step and every later step until this report were "
+              "skipped; parameters unchanged by them");
+    return LCAE_ERR_DATA;
+  }
+  set_error("non-finite loss (SPEC.md:95): the parameters of that step were updated (non-finite); every later "
+            "step until this report was skipped");
+  return LCAE_ERR_NUMERIC;
+}
+
+static lcae_status sync_flags(lcae_layer *L) {
+  LCAE_CK(cudaMemcpyAsync(L->flags_host, L->flags_dev, 2 * sizeof(int), cudaMemcpyDeviceToHost, L->st));
+  LCAE_CK(cudaStreamSynchronize(L->st));
+  return flag_status(L);
+}
+
 static lcae_status read_loss(lcae_layer *L, double *loss) {
   LCAE_CK(cudaMemcpyAsync(L->loss_host, L->loss_dev, 2 * sizeof(double), cudaMemcpyDeviceToHost, L->st));
+  LCAE_CK(cudaMemcpyAsync(L->flags_host, L->flags_dev, 2 * sizeof(int), cudaMemcpyDeviceToHost, L->st));
   LCAE_CK(cudaStreamSynchronize(L->st));
   double J = L->loss_host[0] + L->loss_host[1];
   if (loss) *loss = J;
-  if (!std::isfinite(J)) {
+  lcae_status s = flag_status(L);
+  if (s) return s;
+  if (!std::isfinite(J)) {   // a forward pass (no update): reported directly, nothing is flagged
     set_error("non-finite loss");
     return LCAE_ERR_NUMERIC;
   }
@@ -136,9 +162,10 @@ lcae_status lcae_destroy(lcae_layer *L) {
                   (void *)L->vb, (void *)L->Wb, (void *)L->x_stage, (void *)L->xt32, (void *)L->xt16,
                   (void *)L->dxt, (void *)L->dx_nhwc, (void *)L->pooled, (void *)L->gW, (void *)L->galpha,
                   (void *)L->gb, (void *)L->loss_part, (void *)L->loss_dev, (void *)L->reinit_dev, (void *)L->step_dev,
-                  (void *)L->rowsq})
+                  (void *)L->rowsq, (void *)L->flags_dev})
     if (p) cudaFree(p);
   if (L->loss_host) cudaFreeHost(L->loss_host);
+  if (L->flags_host) cudaFreeHost(L->flags_host);
   if (L->x_pf) cudaFree(L->x_pf);
   if (L->copy_st) cudaStreamDestroy(L->copy_st);
   if (L->pf_done) cudaEventDestroy(L->pf_done);
@@ -209,6 +236,10 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
   CKF(cudaMalloc(&L->step_dev, sizeof(int64_t)));
   CKF(cudaMemsetAsync(L->step_dev, 0, sizeof(int64_t), L->st));
   CKF(cudaMallocHost(&L->loss_host, 2 * sizeof(double)));
+  CKF(cudaMalloc(&L->flags_dev, 2 * sizeof(int)));
+  CKF(cudaMemsetAsync(L->flags_dev, 0, 2 * sizeof(int), L->st));
+  CKF(cudaMallocHost(&L->flags_host, 2 * sizeof(int)));
+  L->flags_host[0] = L->flags_host[1] = 0;
   if (cfg->keep_grads) {
     CKF(cudaMalloc(&L->gW, F * k * wp * 4));
     CKF(cudaMemsetAsync(L->gW, 0, F * k * wp * 4, L->st));
@@ -246,6 +277,7 @@ lcae_status lcae_set_params(lcae_layer *L, const float *W, const float *alpha, c
   }
   if (alpha && (s = copy_any(L, L->alpha, alpha, (size_t)g.F * 4))) return s;
   if (b && (s = copy_any(L, L->b, b, (size_t)g.F * g.n * 4))) return s;
+  LCAE_CK(cudaMemsetAsync(L->flags_dev, 0, 2 * sizeof(int), L->st));   // fresh parameters: flags cleared
   LCAE_CK(cudaStreamSynchronize(L->st));
   return LCAE_OK;
 }
@@ -306,7 +338,7 @@ static lcae_status run(lcae_layer *L, const float *x, bool update, float *dx, fl
   if (pooled && (s = copy_any(L, pooled, L->pooled, (size_t)g.m * g.F * (g.k / g.g) * 4))) return s;
   if (loss || (dx && !is_device_ptr(dx)) || (pooled && !is_device_ptr(pooled))) {
     if (loss) return read_loss(L, loss);
-    LCAE_CK(cudaStreamSynchronize(L->st));
+    return sync_flags(L);
   }
   return LCAE_OK;
 }
@@ -352,6 +384,40 @@ lcae_status lcae_last_loss(lcae_layer *L, double *j_rec, double *j_sparse) {
   LCAE_CK(cudaStreamSynchronize(L->st));
   if (j_rec) *j_rec = L->loss_host[0];
   if (j_sparse) *j_sparse = L->loss_host[1];
+  return LCAE_OK;
+}
+
+lcae_status lcae_sync(lcae_layer *L) {
+  if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
+  return sync_flags(L);
+}
+
+lcae_status lcae_field_losses(lcae_layer *L, double *out) {
+  if (!L || !out) { set_error("NULL argument"); return LCAE_ERR_ARG; }
+  const Geo &g = L->geo;
+  const bool tcp = L->cfg.precision == LCAE_BF16;
+  const int per = tcp ? tc_loss_count(L) / g.F : 1;   // partials per field (CTAs of a cluster)
+  double *part = tcp ? tc_loss_part(L) : L->loss_part;
+  double *h = nullptr;
+  const size_t bytes = (size_t)g.F * per * 2 * sizeof(double);
+  LCAE_CK(cudaMallocHost(&h, bytes));
+  cudaError_t e = cudaMemcpyAsync(h, part, bytes, cudaMemcpyDeviceToHost, L->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(L->st);
+  if (e != cudaSuccess) {
+    cudaFreeHost(h);
+    set_error(std::string("lcae_field_losses: ") + cudaGetErrorString(e));
+    return LCAE_ERR_CUDA;
+  }
+  std::vector<double> tmp((size_t)g.F * 2);
+  for (int f = 0; f < g.F; ++f)
+    for (int q = 0; q < 2; ++q) {
+      double a = 0.0;
+      for (int c = 0; c < per; ++c) a += h[((size_t)f * per + c) * 2 + q];
+      tmp[(size_t)f * 2 + q] = a;
+    }
+  cudaFreeHost(h);
+  if (is_device_ptr(out)) LCAE_CK(cudaMemcpy(out, tmp.data(), tmp.size() * sizeof(double), cudaMemcpyHostToDevice));
+  else memcpy(out, tmp.data(), tmp.size() * sizeof(double));
   return LCAE_OK;
 }
 

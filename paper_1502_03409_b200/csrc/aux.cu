@@ -6,16 +6,21 @@ namespace lcae {
 namespace {
 
 // NHWC [m][P] -> HWCN [P][m] (P = H*W*C): 32x32 tiled transpose through shared memory.
+// Any non-finite input element sets flag[0] ("non-finite ... error"; include/lcae.h LCAE_ERR_DATA).
 template <typename T>
-__global__ void nhwc_to_hwcn(const float *__restrict__ x, T *__restrict__ xt, int m, int mp, int64_t P) {
+__global__ void nhwc_to_hwcn(const float *__restrict__ x, T *__restrict__ xt, int m, int mp, int64_t P, int *flag) {
   __shared__ float tile[32][33];
   const int64_t p0 = (int64_t)blockIdx.x * 32;
   const int i0 = blockIdx.y * 32;
+  bool bad = false;
   for (int r = threadIdx.y; r < 32; r += 8) {
     int i = i0 + r;
     int64_t p = p0 + threadIdx.x;
-    tile[r][threadIdx.x] = (i < m && p < P) ? x[(int64_t)i * P + p] : 0.f;
+    const float v = (i < m && p < P) ? x[(int64_t)i * P + p] : 0.f;
+    bad |= !isfinite(v);
+    tile[r][threadIdx.x] = v;
   }
+  if (bad) flag[0] = 1;
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += 8) {
     int64_t p = p0 + r;
@@ -31,20 +36,23 @@ __global__ void nhwc_to_hwcn(const float *__restrict__ x, T *__restrict__ xt, in
 // Vectorised 64 x 64 variants (16-byte global accesses on both sides; used when P % 4 == 0):
 // NHWC f32 [m][P] -> HWCN bf16 [P][mp] (sample rows in [m, mp) written as zeros).
 __global__ void __launch_bounds__(256) nhwc_to_hwcn_bf16_v(const float *__restrict__ x, __nv_bfloat16 *__restrict__ xt,
-                                                           int m, int mp, int64_t P) {
+                                                           int m, int mp, int64_t P, int *flag) {
   __shared__ float tile[64][65];   // [sample][pixel-feature]
   const int64_t p0 = (int64_t)blockIdx.x * 64;
   const int i0 = blockIdx.y * 64, t = threadIdx.x;
+  bool bad = false;
   for (int r = t / 16; r < 64; r += 16) {   // 16 lanes x float4 = 64 pixel-features of one sample
     const int i = i0 + r, c4 = t % 16;
     const int64_t p = p0 + 4 * c4;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i < m && p < P) v = __ldg(reinterpret_cast<const float4 *>(x + (int64_t)i * P + p));
+    bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
     tile[r][4 * c4] = v.x;
     tile[r][4 * c4 + 1] = v.y;
     tile[r][4 * c4 + 2] = v.z;
     tile[r][4 * c4 + 3] = v.w;
   }
+  if (bad) flag[0] = 1;   // benign race: every writer stores the same value
   __syncthreads();
   for (int q = t / 8; q < 64; q += 32) {   // 8 lanes x 8 bf16 = 64 samples of one pixel-feature
     const int g8 = t % 8, i = i0 + 8 * g8;
@@ -106,9 +114,11 @@ __global__ void hwcn_to_nhwc(const float *__restrict__ xt, float *__restrict__ x
   }
 }
 
-// Fixed-order fp64 reduction of the per-field loss partials [F][2] -> loss[2].
+// Fixed-order fp64 reduction of the per-field loss partials [F][2] -> loss[2]. A step skipped because an error
+// flag was set (flags[0] by this step's staging, or either flag earlier; flags[1] is only set here) does not
+// count; a non-finite loss sets flags[1].
 __global__ void __launch_bounds__(1024) loss_reduce(const double *part, int F, double *out, int64_t *step_dev,
-                                                    int update) {  // F = #partial pairs
+                                                    int update, int *flags) {
   __shared__ double sh[32];
   double a = 0.0, b = 0.0;
   const double2 *p2 = reinterpret_cast<const double2 *>(part);   // [F] pairs, 16-byte aligned (cudaMalloc)
@@ -120,7 +130,10 @@ __global__ void __launch_bounds__(1024) loss_reduce(const double *part, int F, d
   if (threadIdx.x == 0) {
     out[0] = ta;
     out[1] = tb;
-    if (update) ++*step_dev;   // after this step's finalize (stream order), before the next step's
+    if (!(flags[0] | flags[1])) {
+      if (!isfinite(ta + tb)) flags[1] = 1;
+      if (update) ++*step_dev;   // after this step's finalize (stream order), before the next step's
+    }
   }
 }
 
@@ -180,18 +193,13 @@ __global__ void region_add(float *dst, int dst_h, int dst_w, const float *src, i
   }
 }
 
-__global__ void check_finite(const float *x, int64_t n, int *flag) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
-    if (!isfinite(x[t])) { *flag = 1; return; }
-}
-
 }  // namespace
 
 lcae_status launch_nhwc_to_hwcn_f32(lcae_layer *L, const float *x, float *xt) {
   const Geo &g = L->geo;
   int64_t P = (int64_t)g.H * g.W * g.C;
   dim3 grid((unsigned)cdiv((int)P, 32), cdiv(g.m, 32));
-  nhwc_to_hwcn<float><<<grid, dim3(32, 8), 0, L->st>>>(x, xt, g.m, L->mp, P);
+  nhwc_to_hwcn<float><<<grid, dim3(32, 8), 0, L->st>>>(x, xt, g.m, L->mp, P, L->flags_dev);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }
@@ -201,12 +209,12 @@ lcae_status launch_nhwc_to_hwcn_bf16(lcae_layer *L, const float *x, __nv_bfloat1
   int64_t P = (int64_t)g.H * g.W * g.C;
   if (P % 4 == 0 && L->mp % 8 == 0 && ((uintptr_t)x & 15) == 0) {
     dim3 gv((unsigned)((P + 63) / 64), (unsigned)cdiv(g.m, 64));
-    nhwc_to_hwcn_bf16_v<<<gv, 256, 0, L->st>>>(x, xt, g.m, L->mp, P);
+    nhwc_to_hwcn_bf16_v<<<gv, 256, 0, L->st>>>(x, xt, g.m, L->mp, P, L->flags_dev);
     LCAE_CK_LAUNCH(L);
     return LCAE_OK;
   }
   dim3 grid((unsigned)cdiv((int)P, 32), cdiv(g.m, 32));
-  nhwc_to_hwcn<__nv_bfloat16><<<grid, dim3(32, 8), 0, L->st>>>(x, xt, g.m, L->mp, P);
+  nhwc_to_hwcn<__nv_bfloat16><<<grid, dim3(32, 8), 0, L->st>>>(x, xt, g.m, L->mp, P, L->flags_dev);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }
@@ -229,7 +237,7 @@ lcae_status launch_hwcn_to_nhwc_f32(lcae_layer *L, const float *xt, float *x) {
 lcae_status launch_loss_reduce(lcae_layer *L, bool update) {
   const bool tcp = L->cfg.precision == LCAE_BF16;
   loss_reduce<<<1, 1024, 0, L->st>>>(tcp ? tc_loss_part(L) : L->loss_part, tcp ? tc_loss_count(L) : L->geo.F,
-                                     L->loss_dev, L->step_dev, update ? 1 : 0);
+                                     L->loss_dev, L->step_dev, update ? 1 : 0, L->flags_dev);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }
@@ -259,12 +267,6 @@ lcae_status launch_get_W(lcae_layer *L, float *Wout) {
 lcae_status launch_refresh_shadow(lcae_layer *L) {
   if (!L->Wb) return LCAE_OK;
   shadow_w<<<L->sm_count * 8, 256, 0, L->st>>>(L->geo, 128, L->n_al, L->wp, L->W, L->Wb);
-  LCAE_CK_LAUNCH(L);
-  return LCAE_OK;
-}
-
-lcae_status launch_check_finite(lcae_layer *L, const float *x, int64_t count, int *flag) {
-  check_finite<<<L->sm_count * 4, 256, 0, L->st>>>(x, count, flag);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }

@@ -84,6 +84,10 @@ struct lcae_layer {
   double *loss_part = nullptr, *loss_dev = nullptr, *loss_host = nullptr;
   int *reinit_dev = nullptr;   // degenerate rows re-initialised (device counter)
   int64_t *step_dev = nullptr;   // steps taken (device counter: CUDA-graph replays stay exact)
+  // sticky error flags (device): [0] non-finite input seen by the staging kernel, [1] non-finite loss. While
+  // either is set every parameter-updating kernel returns without writing; lcae_sync / a loss read reports and
+  // clears them (include/lcae.h "Errors").
+  int *flags_dev = nullptr, *flags_host = nullptr;
   float *rowsq = nullptr;      // [F][k] row sums of squares of the updated W~ (bf16 mode)
   int64_t steps = 0;
   int launches = 0;
@@ -148,6 +152,5 @@ lcae_status launch_init_params(lcae_layer *L);
 lcae_status launch_fill(lcae_layer *L, float *p, int64_t n, float v);
 lcae_status launch_get_W(lcae_layer *L, float *Wout);   // sigma (.) W~ -> dense [F][k][n]
 lcae_status launch_refresh_shadow(lcae_layer *L);       // W~ -> bf16 shadow
-lcae_status launch_check_finite(lcae_layer *L, const float *x, int64_t count, int *flag);
 
 }  // namespace lcae

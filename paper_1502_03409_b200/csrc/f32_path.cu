@@ -207,9 +207,10 @@ __global__ void col2im_f32(Geo g, int f0, int Fc, const float *dXp, float *dxt) 
 // v = mu v - lr dW; W' = W + v; W' /= ||W'|| (degenerate rows re-initialised).
 __global__ void __launch_bounds__(256) update_w_f32(Geo g, int f0, float *W, const float *dW, float *vW, float lr,
                                                     float mu, uint64_t seed, const int64_t *step_dev, int row0, int col0,
-                                                    int ggc, int *reinit) {
+                                                    int ggc, int *reinit, const int *flags) {
   __shared__ double sh[32];
   __shared__ float s_scale;
+  if (flags[0] | flags[1]) return;   // flagged error: parameters frozen (include/lcae.h "Errors")
   const int b = blockIdx.x, j = blockIdx.y, f = f0 + b, n = g.n;
   float *w = W + ((int64_t)f * g.k + j) * n;
   const float *d = dW + ((int64_t)b * g.k + j) * n;
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(256) update_w_f32(Geo g, int f0, float *W, con
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
       double u = (double)(splitmix64(key + (uint64_t)t) >> 40) / 16777216.0 - 0.5;
       w[t] = (float)u;
+      if (v) v[t] = 0.f;   // a fresh row starts at rest (no stale velocity)
       a2 += u * u;
     }
     double tt = block_sum_f64(a2, sh);
@@ -245,7 +247,8 @@ __global__ void __launch_bounds__(256) update_w_f32(Geo g, int f0, float *W, con
 }
 
 __global__ void update_ab_f32(Geo g, int f0, int Fc, float *alpha, float *bvec, const float *da, const float *db,
-                              float *va, float *vb, float lr, float mu, float amin) {
+                              float *va, float *vb, float lr, float mu, float amin, const int *flags) {
+  if (flags[0] | flags[1]) return;
   int64_t tot = (int64_t)Fc * g.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
     int b = (int)(t / g.n), row = (int)(t - (int64_t)b * g.n), f = f0 + b;
@@ -342,10 +345,10 @@ lcae_status f32_step(lcae_layer *L, bool update, bool want_pooled) {
     // projected SGD update of this chunk's fields
     update_w_f32<<<dim3(Fc, k), 256, 0, L->st>>>(g, f0, L->W, s.dW, L->vW, L->cfg.lr, L->cfg.momentum, L->cfg.seed,
                                                  L->step_dev, L->cfg.field_row0, L->cfg.field_col0,
-                                                 L->cfg.global_grid_c, L->reinit_dev);
+                                                 L->cfg.global_grid_c, L->reinit_dev, L->flags_dev);
     LCAE_CK_LAUNCH(L);
     update_ab_f32<<<256, 256, 0, L->st>>>(g, f0, Fc, L->alpha, L->b, s.da, s.db, L->va, L->vb, L->cfg.lr,
-                                          L->cfg.momentum, L->cfg.alpha_min);
+                                          L->cfg.momentum, L->cfg.alpha_min, L->flags_dev);
     LCAE_CK_LAUNCH(L);
   }
 #undef TRY

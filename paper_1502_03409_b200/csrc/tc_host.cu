@@ -16,10 +16,12 @@ __global__ void __launch_bounds__(128) finalize_kernel(Geo g, int CB, int n_al, 
                                                        float *bvec, float *sigma, float *W, __nv_bfloat16 *Wb,
                                                        float *va, float *vb, float lr, float mu, float amin,
                                                        float *galpha, float *gb, uint64_t seed, const int64_t *step_dev,
-                                                       int row0, int col0, int ggc, int *reinit) {
+                                                       int row0, int col0, int ggc, int *reinit, float *vW, int wp,
+                                                       const int *flags) {
   __shared__ double sh[32];
   __shared__ int bad[KP];
   __shared__ int nbad;
+  if (flags[0] | flags[1]) return;   // the step kernel skipped this step (include/lcae.h "Errors")
   const int f = blockIdx.x, n = g.n, k = g.k;
   if (threadIdx.x == 0) {
     float da = 0.f;
@@ -93,6 +95,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(Geo g, int CB, int n_al, 
       float w = (float)u * s_inv;
       W[((int64_t)f * k + r) * n_al + t] = w;   // W~ rows use the same 16-byte pitch as the shadow
       Wb[((int64_t)f * KP + r) * n_al + t] = __float2bfloat16_rn(w);
+      if (vW) vW[((int64_t)f * k + r) * wp + t] = 0.f;   // a fresh row starts at rest (no stale velocity)
     }
     __syncthreads();
   }
@@ -124,7 +127,10 @@ lcae_status tc_alloc(lcae_layer *L) {
   s->CB = cdiv(g.m, tc::MC);
   s->T = T;
   s->smem = sizeof(tc::Smem) + 1024;
-  const int ncl = std::max(1, std::min(g.F, L->sm_count / s->CB));
+  int ncl = std::max(1, std::min(g.F, L->sm_count / s->CB));
+  // test hook: LCAE_DEV_MAX_CLUSTERS caps the persistent grid so that small layers run several fields per CTA
+  // (the cross-field barrier phases and buffer reuse of the production kernel, checked against the oracle)
+  if (const char *e = getenv("LCAE_DEV_MAX_CLUSTERS")) ncl = std::max(1, std::min(ncl, atoi(e)));
   s->grid = ncl * s->CB;
   LCAE_CK(cudaMalloc(&s->loss_part, (size_t)g.F * s->CB * 2 * sizeof(double)));
   LCAE_CK(cudaMalloc(&s->da_part, (size_t)g.F * s->CB * 4));
@@ -220,6 +226,7 @@ lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_on
   P.dbscr = s->dbscr;
   P.dscr = s->dscr;
   P.gW = L->gW;
+  P.flags = L->flags_dev;
   P.trace = s->trace_on ? s->trace : nullptr;
   if (update) LCAE_CK(cudaMemsetAsync(L->dxt, 0, (size_t)g.H * g.W * g.C * L->mp * 4, L->st));
   cudaLaunchConfig_t cfg = {};
@@ -259,7 +266,7 @@ lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_on
         g, s->CB, L->n_al, s->da_part, s->db_part, s->rowsq_part, L->alpha, L->b, L->sigma, L->W, L->Wb, L->va,
         L->vb, L->cfg.lr, L->cfg.momentum, L->cfg.alpha_min, L->cfg.keep_grads ? L->galpha : nullptr,
         L->cfg.keep_grads ? L->gb : nullptr, L->cfg.seed, L->step_dev, L->cfg.field_row0, L->cfg.field_col0,
-        L->cfg.global_grid_c, L->reinit_dev);
+        L->cfg.global_grid_c, L->reinit_dev, L->vW, L->wp, L->flags_dev);
     LCAE_CK_LAUNCH(L);
   }
   return LCAE_OK;

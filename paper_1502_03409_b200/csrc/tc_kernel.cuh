@@ -75,6 +75,7 @@ struct Params {
   float *dbscr;        // [grid][4][MAX_NPAD]: per-lane-quarter db partials of the current field
   uint8_t *dscr;       // [grid][T][16 KB]: pass-1 delta tiles (their swizzled smem image), reloaded in pass 2
   float *gW;
+  const int *flags;   // sticky error flags (non-finite input / loss): a training step does nothing while set
   unsigned long long *trace;   // nullable: per-role wait cycles summed over CTAs
 };
 
@@ -183,6 +184,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
   const bool step = GEN ? P.mode == 1 : true;
   const bool enc = GEN && P.mode == 2;   // encode-only inference (pass 0 + pooling)
   const bool want_pooled = GEN && P.want_pooled;
+  // a flagged error (this step's input had a non-finite value, or an earlier loss was non-finite) freezes the
+  // parameters: every CTA reads the same flags (written by earlier kernels), so all return together
+  if (step && (P.flags[0] | P.flags[1])) return;
   // trace: lane 0 of the producers / MMA warp and of epilogue warp 2 record their barrier-wait cycles
   const bool trec = TR && P.trace != nullptr && lane == 0 && (warp <= 2 || warp == XWARP);
   const long long t_start = clock64();

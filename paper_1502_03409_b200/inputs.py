@@ -7,8 +7,10 @@ configs and how to draw seeded inputs of those shapes:
 * images  X : [m][H][W][C] float32, i.i.d. N(0,1) per pixel (the synthetic
   analogue of the paper's whitened patches, "whitened as in
   [coates13]"), standardised per image and channel (SPEC.md:424-432
-  standardize_image), then rounded to bf16-representable float32 so that the
-  fp32 and bf16 device paths and the fp64 oracle all see identical values.
+  standardize_image), then (by default) rounded to bf16-representable float32
+  so that the fp32 and bf16 device paths and the fp64 oracle all see identical
+  values; ``bf16_round=False`` keeps the raw float32 values (the bf16 path then
+  rounds x itself, and the parity tests measure that rounding too).
 * params  W : [F][k][n] float32, Gaussian rows normalised to unit length
   (PAPER.md:89 "subject to ||W^(k)||_2 = 1"); alpha = alpha_init; b = 0.
   Each field draws from its own SeedSequence([seed, 0x57, f]) so any subset
@@ -84,15 +86,16 @@ def round_to_bf16(a: np.ndarray) -> np.ndarray:
 
 
 def make_images(shape: LayerShape, seed: int = 1, index: int = 0,
-                batch: Optional[int] = None) -> np.ndarray:
-    """Seeded whitened-like image batch, NHWC float32 [m][H][W][C], bf16-representable."""
+                batch: Optional[int] = None, bf16_round: bool = True) -> np.ndarray:
+    """Seeded whitened-like image batch, NHWC float32 [m][H][W][C] (bf16-representable unless bf16_round=False)."""
     m = shape.batch if batch is None else batch
     rng = np.random.default_rng(np.random.SeedSequence([seed, 0x1A, index]))
     x = rng.standard_normal((m, shape.img_h, shape.img_w, shape.img_c))
     mu = x.mean(axis=(1, 2), keepdims=True)
     sd = x.std(axis=(1, 2), keepdims=True)
     x = (x - mu) / np.maximum(sd, 1e-12)
-    return round_to_bf16(x.astype(np.float32))
+    x = x.astype(np.float32)
+    return round_to_bf16(x) if bf16_round else x
 
 
 def make_field_weights(shape: LayerShape, fields: Iterable[int], seed: int = 0) -> np.ndarray:

@@ -13,7 +13,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LCAE_LIB") or os.path.join(_HERE, "liblcae.so")  # LCAE_LIB: A/B another build
 
-LCAE_OK, LCAE_ERR_CONFIG, LCAE_ERR_DATA, LCAE_ERR_NUMERIC, LCAE_ERR_CUDA, LCAE_ERR_ARG = 0, 2, 3, 4, 5, 7
+LCAE_OK, LCAE_ERR_CONFIG, LCAE_ERR_DATA, LCAE_ERR_NUMERIC, LCAE_ERR_CUDA, LCAE_ERR_NCCL, LCAE_ERR_ARG = 0, 2, 3, 4, 5, 6, 7
 FP32, BF16 = 0, 1
 
 
@@ -58,6 +58,8 @@ def _load():
         "lcae_lcn": (C.c_int, [P, P, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, P]),
         "lcae_topk_update": (C.c_int, [P, C.c_int64, C.c_int64, C.c_int32, C.c_int64, P, P, P]),
         "lcae_last_loss": (C.c_int, [P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "lcae_sync": (C.c_int, [P]),
+        "lcae_field_losses": (C.c_int, [P, P]),
         "lcae_dx_device": (C.c_int, [P, C.POINTER(P)]),
         "lcae_counters": (C.c_int, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
         "lcae_region_add": (C.c_int, [P, P, C.c_int32, C.c_int32, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
@@ -86,6 +88,7 @@ lib = _load()
 # Every symbol include/lcae.h declares (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("lcae_config_default", "lcae_geometry", "lcae_create", "lcae_destroy", "lcae_set_params",
                "lcae_get_params", "lcae_get_grads", "lcae_forward", "lcae_encode", "lcae_step", "lcae_last_loss",
+               "lcae_sync", "lcae_field_losses",
                "lcae_topk_init", "lcae_topk_update", "lcae_lcn", "lcae_prefetch_input",
                "lcae_dx_device", "lcae_counters", "lcae_region_add", "lcae_last_launch_count",
                "lcae_profile", "lcae_profile_read",
@@ -192,6 +195,16 @@ class Layer:
         a, b = C.c_double(), C.c_double()
         check(lib.lcae_last_loss(self.h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def sync(self):
+        """Wait for the layer's stream; raises LcaeError (DATA / NUMERIC) for a flagged non-finite input / loss."""
+        check(lib.lcae_sync(self.h))
+
+    def field_losses(self) -> np.ndarray:
+        """[F][2] float64: per-field (J_rec, J_sparse) of the last step / forward."""
+        out = np.zeros((self.F, 2), np.float64)
+        check(lib.lcae_field_losses(self.h, out.ctypes.data))
+        return out
 
     def dx_device_ptr(self) -> int:
         p = C.c_void_p()

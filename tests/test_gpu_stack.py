@@ -44,6 +44,8 @@ def _oracle_chain(cfg, params, X):
 
 
 def test_stack_forward_matches_oracle_chain_fp32():
+    """Each stage of the fp32 forward chain (encode, LCN, encode, LCN, encode) against the oracle on the GPU
+    stage's own input, at north_star's 1e-5; and the whole chain against the all-oracle chain at 1e-5."""
     import torch
     from paper_1502_03409_b200 import lcae
     from paper_1502_03409_b200.stack import Stack, desk_stack
@@ -51,13 +53,27 @@ def test_stack_forward_matches_oracle_chain_fp32():
     X = make_images(cfg.shapes[0], seed=1)
     params = [make_params(s, seed=i) for i, s in enumerate(cfg.shapes)]
     st = Stack(cfg, precision=lcae.FP32, seed=0)
+    errs = {}
     try:
+        x = torch.from_numpy(X).cuda()
+        for l, s in enumerate(cfg.shapes):
+            code = st._code(l, x)
+            W, a, b = params[l]
+            want = layer_gradients(W.astype(np.float64), a.astype(np.float64), b.astype(np.float64),
+                                   x.cpu().numpy().astype(np.float64), geo_of(s))["p"]
+            errs[f"encode{l}"] = normwise(code.cpu().numpy(), want)
+            if l + 1 < len(cfg.shapes):
+                x = st._lcn(code)
+                errs[f"lcn{l}"] = normwise(x.cpu().numpy(), lcn(code.cpu().numpy().astype(np.float64),
+                                                               cfg.lcn_window, cfg.lcn_floor))
         top = st.forward(torch.from_numpy(X).cuda()).cpu().numpy()
     finally:
         st.close()
     want = _oracle_chain(cfg, params, X)[-1]
     assert top.shape == want.shape == (8, 1, 1, 16)
-    assert normwise(top, want) <= 1e-4
+    errs["chain"] = normwise(top, want)
+    print({k: f"{v:.1e}" for k, v in errs.items()})
+    assert all(v <= 1e-5 for v in errs.values()), errs
 
 
 def test_greedy_layer_steps_match_oracle_bf16():
