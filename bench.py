@@ -6,8 +6,10 @@ images/sec per LC-autoencoder training step, TFLOP/s vs B200 peak).
 A step = one pass of the whole hot path (input staging, encode, L2 pooling +
 sparsity, decode + residual, loss reduction, backprop into the code, weight gradient, input gradient with
 overlap-add, fused projected-SGD update) over one batch of synthetic whitened images, through the C ABI.
-N = 1: the whole layer on one GPU.  N > 1 (torchrun): the field grid is tiled over ranks (parallel.py);
-every rank runs its tile, halos travel over NCCL; value = images/s of the whole job (model parallel: every
+N = 1: the whole layer on one GPU.  N > 1 (torchrun): the field grid is tiled over ranks inside the library
+(include/lcae.h world_size > 1, csrc/mp.cu): every rank runs its tile, the input halo (bf16) and the dX
+return travel by NCCL send/recv on the layer's comm stream while the interior fields compute, the loss is
+all-reduced; value = images/s of the whole job (model parallel: every
 rank sees every image), time = max over ranks.
 
 --impl reference: the fp64 CPU oracle (oracle/), as it stands, timed on this host on a bounded sample of
@@ -49,6 +51,20 @@ def alg_bytes(shape):
     w = shape.fields * shape.filters * shape.n
     x = shape.batch * shape.img_h * shape.img_w * shape.img_c
     return 8.0 * w * (2 if shape.momentum > 0 else 1) + 8.0 * shape.fields * (shape.n + 1) + 2.0 * x + 4.0 * x
+
+
+def executed_flops(shape):
+    """FLOPs the tcgen05 MMAs of the fused step kernel execute: filters padded to KP = 128, patch
+    rows to 64-row tiles, samples to 128 per CTA, plus the exact -I tiles of the residual and dX products."""
+    KP, NT, MC = 128, 64, 128
+    T = -(-shape.n // NT)
+    CB = -(-shape.batch // MC)
+    per_cta = (2 * MC * KP * T * NT                       # pass 0: U^T = X^T W~^T
+               + 2 * MC * NT * (KP + NT) * T                # pass 1: R^T - X^T = H'^T W~_j + X_j^T (-I)
+               + 2 * MC * KP * NT * T                       # pass 1: G^T += delta_j^T W~_j^T
+               + 2 * MC * NT * (KP + NT) * T                # pass 2: dx^T = D'^T W~_j + delta_j^T (-I)
+               + 2 * KP * NT * 2 * MC * T)                  # pass 2: dW_j = H' delta_j^T + D' X_j^T
+    return float(per_cta) * CB * shape.fields
 
 
 def model_flops(shape):
@@ -291,22 +307,32 @@ def run_ours(args, shape):
     dist = None
     stream = torch.cuda.Stream()
     pk = peaks()
+    nid = None
     if world > 1:
+        # model parallel inside the library (include/lcae.h world_size > 1): rank 0 creates the NCCL id, the
+        # process group (plumbing) broadcasts it; halos, dX returns and the loss all-reduce are the library's
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        from paper_1502_03409_b200 import parallel
-        tile = parallel.plan(shape, world)[rank]
-        with torch.cuda.stream(stream):
-            runner = parallel.TileRunner(shape, tile, world, rank, stream=stream.cuda_stream)
+        obj = [lcae.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
     with torch.cuda.stream(stream):
-        if world == 1:
-            cfg = lcae.make_config(shape, precision=lcae.BF16, stream=stream.cuda_stream)
+        if True:
+            cfg = lcae.make_config(shape, precision=lcae.BF16, stream=stream.cuda_stream, world_size=world,
+                                   rank=rank, nccl_id=nid)
             L = lcae.Layer(cfg)
-            if shape.fields * shape.filters * shape.n < DEVICE_INIT_PARAMS:
-                W, a, b = make_params(shape, seed=0)
+            if world > 1:
+                R0, R1, C0, C1 = L.own_fields
+                mine = [r * shape.grid_c + c for r in range(R0, R1) for c in range(C0, C1)]
+                y0, y1, x0, x1 = L.own_px
+            else:
+                mine, (y0, y1, x0, x1) = None, (0, shape.img_h, 0, shape.img_w)
+            if L.F * shape.filters * shape.n < DEVICE_INIT_PARAMS:
+                W, a, b = make_params(shape, seed=0, fields=mine)
                 L.set_params(W, a, b)
                 del W
-            pool = [torch.from_numpy(make_images(shape, seed=1, index=i)).cuda() for i in range(4)]
+            pool = [torch.from_numpy(np.ascontiguousarray(
+                make_images(shape, seed=1, index=i)[:, y0:y1, x0:x1, :])).cuda() for i in range(4)]
             step = lambda i: L.step(pool[i % len(pool)], None, want_loss=False)  # noqa: E731
             if args.graph:   # one CUDA graph per pool entry (launch-bound small configs)
                 torch.cuda.synchronize()
@@ -318,14 +344,11 @@ def run_ours(args, shape):
                     graphs.append(gph)
                 eager_step = step
                 step = lambda i: graphs[i % len(graphs)].replay()  # noqa: E731
-        else:
-            L = runner.layer
-            step = runner.bench_step_fn(stream)
         torch.cuda.synchronize()
         for i in range(args.warmup):
             step(i)
         torch.cuda.synchronize()
-        launches_per_step = L.last_launch_count() + (runner.extra_launches if world > 1 else 0)
+        launches_per_step = L.last_launch_count()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -343,6 +366,7 @@ def run_ours(args, shape):
         L.profile(False)
         ms = e0.elapsed_time(e1)
         kern_ms, kern_n = L.profile_read()
+        prof_steps = args.steps   # model parallel: two step-kernel launches per step (interior, boundary)
         if world == 1 and args.graph:   # graph replays carry no profile events: time the kernel on eager steps
             L.profile(True)
             for i in range(10):
@@ -350,6 +374,7 @@ def run_ours(args, shape):
             torch.cuda.synchronize()
             L.profile(False)
             kern_ms, kern_n = L.profile_read()
+            prof_steps = 10
         if dist:
             t = torch.tensor([ms, kern_ms], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -357,7 +382,7 @@ def run_ours(args, shape):
         ms_step = ms / args.steps
         # ---- end to end through the C ABI with host buffers (pinned), loss read back every step
         e2e = None
-        if world == 1:
+        if True:
             hosts = [p.cpu().pin_memory() for p in pool[:2]]
             h2d = hosts[0].numel() * 4
             # warm-up through the same path (the first lcae_prefetch_input allocates its buffer, stream, events)
@@ -381,17 +406,34 @@ def run_ours(args, shape):
                 if not np.isfinite(jr + js):
                     raise RuntimeError("non-finite loss in the e2e loop")
             dt = (time.perf_counter() - t0) / n_e2e
+            if dist:   # the slowest rank bounds the job
+                t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                dt = t.item()
+                t = torch.tensor([float(h2d)], device="cuda", dtype=torch.float64)
+                dist.all_reduce(t)   # every rank copies its owned pixels: the job's bytes
+                h2d = int(t.item())
             e2e = {"value": shape.batch / dt, "unit": "images/s", "h2d_bytes_per_step": h2d,
                    "d2h_bytes_per_step": 16, "ms_per_step": dt * 1e3, "h2d_overlap": "lcae_prefetch_input"}
     if rank != 0:
         return
     flops = model_flops(shape)
     value = shape.batch / (ms_step * 1e-3)
-    kern_avg = kern_ms / max(1, kern_n)
+    if args.scaling == "weak":   # the layer grows with N: report base-layer-equivalent images/s (value x F / F_base)
+        value *= shape.fields / args.base_fields
+    kern_avg = kern_ms / max(1, prof_steps)   # step-kernel time per step (all its launches)
     per_kernel_flops = flops / world
     achieved = per_kernel_flops / (kern_avg * 1e-3) / 1e12
     achieved_gbs = alg_bytes(shape) / world / (kern_avg * 1e-3) / 1e9
     hbm_bound = alg_bytes(shape) / (pk["hbm"] * 1e9) > flops / (pk["bf16_sus"] * 1e12)
+    # the denominator follows the clocks seen in the timed region: the burst peak when the SM clock held its
+    # maximum (the kernel ran at full clock), the sustained (power-capped) peak otherwise
+    ck = clk.summary()
+    burst = bool(ck.get("sm_mhz") and ck.get("sm_max_mhz") and ck["sm_mhz"] >= 0.95 * ck["sm_max_mhz"])
+    tc_peak = pk["bf16"] if burst else pk["bf16_sus"]
+    tc_src = (f"{pk['src']} bf16_tflops (burst: SM clock median {ck.get('sm_mhz')} of max {ck.get('sm_max_mhz')} MHz "
+              f"in the timed region)" if burst else
+              f"{pk['src']} bf16_tflops_sustained (SM clock median {ck.get('sm_mhz')} MHz below max)")
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
@@ -402,7 +444,7 @@ def run_ours(args, shape):
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": shape.name, "image": [shape.img_h, shape.img_w, shape.img_c], "rf": shape.rf_h,
                    "stride": shape.stride, "filters": shape.filters, "pool_group": shape.pool_group,
                    "batch": shape.batch, "fields": shape.fields, "params": shape.fields * shape.filters * shape.n,
@@ -415,13 +457,15 @@ def run_ours(args, shape):
                       "kernel": "lcae::tc::step_kernel", "kernel_ms": kern_avg,
                       "peak_source": f"{pk['src']} hbm_gbs", "tensor_frac": achieved / pk["bf16_sus"]}
                      if hbm_bound else
-                     {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
-                      "frac": achieved / pk["bf16_sus"], "traffic": traffic,
-                      "kernel": "lcae::tc::step_kernel", "kernel_ms": kern_avg,
-                      "peak_source": f"{pk['src']} bf16_tflops_sustained (kernel timed inside a long step)",
+                     {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
+                      "frac": achieved / tc_peak, "traffic": traffic,
+                      "kernel": "lcae::tc::step_kernel", "kernel_ms": kern_avg, "peak_source": tc_src,
+                      "frac_of_sustained": achieved / pk["bf16_sus"], "frac_of_burst": achieved / pk["bf16"],
+                      "model_flops_per_step": flops, "executed_flops_per_step": executed_flops(shape),
+                      "executed_tflops": executed_flops(shape) / world / (kern_avg * 1e-3) / 1e12,
                       "hbm_frac": achieved_gbs / pk["hbm"]}),
         "gpu_launches": launches_per_step * args.steps,
-        "clocks": clk.summary(),
+        "clocks": ck,
         "e2e": e2e,
     }
     if not args.no_cpu_baseline and world == 1:
@@ -443,6 +487,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--momentum", type=float, default=0.0, help="SGD momentum (SURVEY.md §8(f) item 3: 0.9)")
     ap.add_argument("--graph", action="store_true", help="replay each step from a captured CUDA graph (1 GPU)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's layer on N GPUs (default); weak: the field grid grows with N "
+                         "(SURVEY.md §8(d) c5: grid_r x grid_c fields per GPU, global grid scaled by the tiles); "
+                         "value = base-layer-equivalent images/s")
     ap.add_argument("--mode", default="train", choices=["train", "infer"],
                     help="train: the training step (default); infer: encode + top-K stimuli (§8(f) item 4)")
     args = ap.parse_args()
@@ -450,6 +498,13 @@ def main():
     shape = CONFIGS[args.config] if args.config in CONFIGS else EXTRA[args.config]
     if args.momentum:
         shape = shape.replace(momentum=args.momentum)
+    args.base_fields = shape.fields
+    if args.scaling == "weak":
+        from paper_1502_03409_b200.parallel import factor
+        tr, tc = factor(int(os.environ.get("WORLD_SIZE", "1")))
+        gr, gc = shape.grid_r * tr, shape.grid_c * tc
+        shape = shape.replace(name=f"{shape.name}-weak", img_h=(gr - 1) * shape.stride + shape.rf_h,
+                              img_w=(gc - 1) * shape.stride + shape.rf_w)
     if args.impl == "reference":
         run_reference(args, shape)
     elif args.mode == "infer":

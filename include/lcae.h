@@ -86,18 +86,62 @@ typedef struct {
   uint64_t seed;               /* degenerate-row re-initialisation generator seed */
   int32_t precision;           /* lcae_precision */
   int32_t keep_grads;          /* 1: also store dW/dalpha/db of the last step for lcae_get_grads (tests) */
-  int32_t field_row0, field_col0, global_grid_c; /* global id of local field (r,c) = (row0+r)*ggc + col0+c */
+  int32_t field_row0, field_col0, global_grid_c; /* global id of local field (r,c) = (row0+r)*ggc + col0+c
+                                                   (caller-tiled mode, world_size == 1; set by the library
+                                                   itself when world_size > 1) */
+  /* Model parallelism over receptive fields inside the library ("model parallel ...
+   * communication ... occurs when a layer's input (or output) field spans multiple GPUs").
+   * world_size > 1: img_h/img_w are the GLOBAL image; the field grid is cut into tiles_r x tiles_c contiguous
+   * rectangles (rank r = tile (r / tiles_c, r % tiles_c); tiles_r = tiles_c = 0 derives the
+   * most square split with tiles_r >= tiles_c); this rank owns the weights of its fields and the pixel
+   * rectangle own_px (lcae_geometry). x / dx of lcae_step / lcae_forward are then this rank's OWNED pixels,
+   * NHWC f32 [m][own_h][own_w][C]; pooled is [m][local grid_r][local grid_c][k/g]; the loss is the global sum.
+   * Each step exchanges the input halo (bf16 on the tensor-core path) and returns the halo dX (fp32) with NCCL
+   * send/recv on the layer's comm stream, the halo overlapping the interior fields; the loss is all-reduced. */
+  int32_t world_size;          /* 1 (default) = one GPU (with nccl_id set: a one-tile model-parallel layer) */
+  int32_t rank;                /* 0 .. world_size-1 */
+  int32_t tiles_r, tiles_c;    /* tiles_r * tiles_c == world_size, or both 0 */
+  const void *nccl_id;         /* 128-byte ncclUniqueId (lcae_nccl_unique_id on one rank, broadcast by the caller);
+                                  NULL with world_size > 1 = test mode: no NCCL, the caller moves the exchange
+                                  buffers between phases (lcae_mp_buffer / lcae_mp_phase) */
   void *stream;                /* cudaStream_t; NULL = default stream */
 } lcae_config;
 
 /* Fill *cfg with the defaults of DESIGN.md (lambda 0.1, eps 1e-6, lr 1e-3, momentum 0, alpha 1, 1e-8). */
 void lcae_config_default(lcae_config *cfg);
 
-/* Validate cfg and report the derived geometry without allocating anything.
- * grid_r/grid_c/n_params may be NULL. n_params = F*(k*n + n + 1).
+/* Validate cfg and report the derived geometry without allocating anything (no GPU needed).
+ * grid_r/grid_c/n_params: THIS rank's field grid and parameter count F*(k*n + n + 1) (the
+ * whole layer when world_size == 1). own_px = {y0, y1, x0, x1}: the global pixel rectangle this rank owns;
+ * own_fields = {R0, R1, C0, C1}: its global field rows / columns. Any output may be NULL.
  * Errors: LCAE_ERR_CONFIG with the residue for non-divisible extents, g not dividing k
- * or 32, rf larger than the image, non-positive sizes, unknown precision. */
-lcae_status lcae_geometry(const lcae_config *cfg, int32_t *grid_r, int32_t *grid_c, int64_t *n_params);
+ * or 32, rf larger than the image, non-positive sizes, unknown precision, a tile without fields,
+ * tiles_r * tiles_c != world_size, rank out of range. */
+lcae_status lcae_geometry(const lcae_config *cfg, int32_t *grid_r, int32_t *grid_c, int64_t *n_params,
+                          int32_t own_px[4], int32_t own_fields[4]);
+
+/* Write a fresh 128-byte ncclUniqueId to out128 (host memory), for lcae_config.nccl_id of every rank.
+ * Errors: LCAE_ERR_NCCL when libnccl.so.2 cannot be loaded or fails. */
+lcae_status lcae_nccl_unique_id(void *out128);
+
+/* Model-parallel test mode (world_size > 1, nccl_id == NULL): a step is three calls, and between them the
+ * caller copies, for every pair of ranks (a, b), a's send buffer for b into b's receive buffer from a:
+ *   lcae_mp_phase(L, 0, x, ...)  stage the owned x, pack the halo neighbours need, run the interior fields;
+ *   -- move input-halo buffers (which 0 -> which 1) --
+ *   lcae_mp_phase(L, 1, ...)     unpack the halo, run the boundary fields, finalize, local loss, pack halo dX;
+ *   -- move dX buffers (which 2 -> which 3) --
+ *   lcae_mp_phase(L, 2, ..., dx, loss)  add the returned dX into the owned pixels, write dx (owned, NHWC f32),
+ *                                       loss = this rank's local J (the caller sums over ranks).
+ * update = 1 trains (lcae_step), 0 = forward (pooled nullable, phases 0-1 only, then 2 for the loss).
+ * lcae_mp_buffer: device pointer and byte size of buffer `which` (0 halo send to peer, 1 halo receive from
+ * peer, 2 dX send to peer, 3 dX receive from peer); NULL / 0 when the pair exchanges nothing. Buffers are
+ * owned by the layer. Errors: ARG (not a model-parallel test-mode layer, bad phase order), CUDA. */
+lcae_status lcae_mp_phase(lcae_layer *L, int32_t phase, int32_t update, const float *x, float *dx, float *pooled,
+                          double *loss);
+lcae_status lcae_mp_buffer(lcae_layer *L, int32_t which, int32_t peer, void **ptr, int64_t *bytes);
+
+/* Interior / boundary field counts of a model-parallel rank (interior fields run while the halo travels). */
+lcae_status lcae_mp_fields(lcae_layer *L, int32_t *n_interior, int32_t *n_boundary);
 
 /* Create a layer on the current CUDA device: validates cfg (as lcae_geometry), allocates parameters,
  * gradient/optimizer state and scratch, and initialises W to unit rows from a counter-based generator,

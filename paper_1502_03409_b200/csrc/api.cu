@@ -16,6 +16,8 @@ static lcae_status config_error(const std::string &m) {
   return LCAE_ERR_CONFIG;
 }
 
+static Geo make_geo(const lcae_config *c, int H, int W);
+
 // Geometry validation (R7) and derived sizes.
 static lcae_status validate(const lcae_config *c, Geo *out) {
   if (!c) { set_error("NULL config"); return LCAE_ERR_ARG; }
@@ -34,8 +36,31 @@ static lcae_status validate(const lcae_config *c, Geo *out) {
   if (c->precision != LCAE_FP32 && c->precision != LCAE_BF16) return config_error("unknown precision");
   if (!(c->eps >= 0.f) || !(c->lr >= 0.f) || !(c->momentum >= 0.f && c->momentum < 1.f) || !(c->alpha_min > 0.f))
     return config_error("eps/lr must be >= 0, momentum in [0,1), alpha_min > 0");
+  if (c->world_size < 0) return config_error("world_size must be >= 1");
+  Geo g = make_geo(c, c->img_h, c->img_w);
+  if ((int64_t)g.H * g.W * g.C * g.m >= (1ll << 31)) return config_error("image x batch too large (>= 2^31 elements)");
+  if (out) *out = g;
+  return LCAE_OK;
+}
+
+// This rank's geometry: the whole layer (world_size <= 1), else the rectangle its tile's fields read (mp.cu).
+static lcae_status local_geo(const lcae_config *c, const Geo &gg, MpTile *t, Geo *out) {
+  if (c->world_size <= 1) {
+    t->R0 = 0; t->R1 = gg.gr; t->C0 = 0; t->C1 = gg.gc;
+    t->need[0] = t->own[0] = 0; t->need[1] = t->own[1] = gg.H;
+    t->need[2] = t->own[2] = 0; t->need[3] = t->own[3] = gg.W;
+    *out = gg;
+    return LCAE_OK;
+  }
+  lcae_status s = mp_tile(c, gg, c->rank, t);
+  if (s) return s;
+  *out = make_geo(c, t->need[1] - t->need[0], t->need[3] - t->need[2]);
+  return LCAE_OK;
+}
+
+static Geo make_geo(const lcae_config *c, int H, int W) {
   Geo g{};
-  g.H = c->img_h; g.W = c->img_w; g.C = c->img_c; g.rf_h = c->rf_h; g.rf_w = c->rf_w; g.s = c->stride;
+  g.H = H; g.W = W; g.C = c->img_c; g.rf_h = c->rf_h; g.rf_w = c->rf_w; g.s = c->stride;
   g.k = c->filters; g.g = c->pool_group; g.m = c->batch;
   g.gr = (g.H - g.rf_h) / g.s + 1;
   g.gc = (g.W - g.rf_w) / g.s + 1;
@@ -45,9 +70,7 @@ static lcae_status validate(const lcae_config *c, Geo *out) {
   g.SY = (int64_t)g.W * g.C * g.m;
   g.SRC_R = (int64_t)g.s * g.SY;
   g.SRC_C = (int64_t)g.s * g.C * g.m;
-  if ((int64_t)g.H * g.W * g.C * g.m >= (1ll << 31)) return config_error("image x batch too large (>= 2^31 elements)");
-  if (out) *out = g;
-  return LCAE_OK;
+  return g;
 }
 
 static bool is_device_ptr(const void *p) {
@@ -62,10 +85,15 @@ static lcae_status copy_any(lcae_layer *L, void *dst, const void *src, size_t by
   return LCAE_OK;
 }
 
+// Elements of the caller's input / dx: the layer image, or this rank's owned pixels (model parallel).
+static size_t input_elems(lcae_layer *L) {
+  const Geo &g = L->geo;
+  return L->mpst ? mp_input_elems(L) : (size_t)g.m * g.H * g.W * g.C;
+}
+
 // Make x device-resident (staging host data) and convert to the path's internal HWCN layout.
 static lcae_status stage_input(lcae_layer *L, const float *x) {
-  const Geo &g = L->geo;
-  size_t bytes = (size_t)g.m * g.H * g.W * g.C * 4;
+  size_t bytes = input_elems(L) * 4;
   const float *xd = x;
   if (L->pf_host && L->pf_host == (const void *)x) {   // prefetched by lcae_prefetch_input
     LCAE_CK(cudaStreamWaitEvent(L->st, L->pf_done, 0));
@@ -76,8 +104,9 @@ static lcae_status stage_input(lcae_layer *L, const float *x) {
     if (s) return s;
     xd = L->x_stage;
   }
-  lcae_status s = (L->cfg.precision == LCAE_FP32) ? launch_nhwc_to_hwcn_f32(L, xd, L->xt32)
-                                                  : launch_nhwc_to_hwcn_bf16(L, xd, L->xt16);
+  lcae_status s = L->mpst ? mp_stage(L, xd)
+                 : (L->cfg.precision == LCAE_FP32) ? launch_nhwc_to_hwcn_f32(L, xd, L->xt32)
+                                                   : launch_nhwc_to_hwcn_bf16(L, xd, L->xt16);
   if (s) return s;
   if (L->x_consumed) LCAE_CK(cudaEventRecord(L->x_consumed, L->st));   // x_pf may be refilled after this
   return LCAE_OK;
@@ -137,18 +166,24 @@ void lcae_config_default(lcae_config *c) {
   c->alpha_min = 1e-8f;
   c->pool_group = 1;
   c->precision = LCAE_BF16;
+  c->world_size = 1;
 }
 
 const char *lcae_last_error(void) { return g_err.c_str(); }
 const char *lcae_version(void) { return "lcae 0.1.0 sm_100a"; }
 
-lcae_status lcae_geometry(const lcae_config *cfg, int32_t *grid_r, int32_t *grid_c, int64_t *n_params) {
-  Geo g;
-  lcae_status s = validate(cfg, &g);
+lcae_status lcae_geometry(const lcae_config *cfg, int32_t *grid_r, int32_t *grid_c, int64_t *n_params,
+                          int32_t own_px[4], int32_t own_fields[4]) {
+  Geo gg, g;
+  MpTile t;
+  lcae_status s = validate(cfg, &gg);
   if (s) return s;
+  if ((s = local_geo(cfg, gg, &t, &g))) return s;
   if (grid_r) *grid_r = g.gr;
   if (grid_c) *grid_c = g.gc;
   if (n_params) *n_params = (int64_t)g.F * ((int64_t)g.k * g.n + g.n + 1);
+  if (own_px) for (int i = 0; i < 4; ++i) own_px[i] = t.own[i];
+  if (own_fields) { own_fields[0] = t.R0; own_fields[1] = t.R1; own_fields[2] = t.C0; own_fields[3] = t.C1; }
   return LCAE_OK;
 }
 
@@ -156,6 +191,7 @@ lcae_status lcae_destroy(lcae_layer *L) {
   if (!L) return LCAE_OK;
   if (L->st) cudaStreamSynchronize(L->st);
   cudaDeviceSynchronize();
+  mp_free(L);
   f32_free(L);
   tc_free(L);
   for (void *p : {(void *)L->W, (void *)L->sigma, (void *)L->alpha, (void *)L->b, (void *)L->vW, (void *)L->va,
@@ -181,11 +217,18 @@ lcae_status lcae_destroy(lcae_layer *L) {
 lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
   if (!out) { set_error("NULL out"); return LCAE_ERR_ARG; }
   *out = nullptr;
-  Geo g;
-  lcae_status s = validate(cfg, &g);
+  Geo gg, g;
+  MpTile tile;
+  lcae_status s = validate(cfg, &gg);
   if (s) return s;
+  if ((s = local_geo(cfg, gg, &tile, &g))) return s;
   lcae_layer *L = new lcae_layer();
   L->cfg = *cfg;
+  if (L->cfg.world_size > 1) {   // the tile's global field offsets key the counter-based init / reinit
+    L->cfg.field_row0 = tile.R0;
+    L->cfg.field_col0 = tile.C0;
+    L->cfg.global_grid_c = gg.gc;
+  }
   if (L->cfg.global_grid_c <= 0) L->cfg.global_grid_c = g.gc;
   L->geo = g;
   L->st = (cudaStream_t)cfg->stream;
@@ -224,7 +267,7 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
   }
   L->mp = cfg->precision == LCAE_FP32 ? g.m : (g.m + 7) / 8 * 8;
   const size_t mp = L->mp;
-  CKF(cudaMalloc(&L->x_stage, m * img * 4));
+  CKF(cudaMalloc(&L->x_stage, m * img * 4));   // >= the owned pixels of a model-parallel rank
   CKF(cudaMalloc(&L->dxt, mp * img * 4));
   CKF(cudaMalloc(&L->dx_nhwc, m * img * 4));
   CKF(cudaMalloc(&L->pooled, m * F * (k / g.g) * 4));
@@ -255,6 +298,9 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
     CKF(cudaMalloc(&L->rowsq, F * k * 4));
     FAIL(tc_alloc(L));
   }
+  // model parallel: world_size > 1; or one rank with an NCCL id (the whole layer as a single tile: exercises the
+  // communicator, the interior / boundary launches and the loss all-reduce on one GPU)
+  if (cfg->world_size > 1 || cfg->nccl_id) FAIL(mp_init(L, gg));
   FAIL(launch_init_params(L));
   FAIL(launch_refresh_shadow(L));
   CKF(cudaStreamSynchronize(L->st));
@@ -325,14 +371,24 @@ static lcae_status run(lcae_layer *L, const float *x, bool update, float *dx, fl
   L->launches = 0;
   const Geo &g = L->geo;
   lcae_status s;
+  if (L->mpst && mp_external(L)) {
+    set_error("model-parallel test-mode layer (nccl_id == NULL): drive it with lcae_mp_phase");
+    return LCAE_ERR_ARG;
+  }
   if ((s = stage_input(L, x))) return s;
-  s = (L->cfg.precision == LCAE_FP32) ? f32_step(L, update, pooled != nullptr)
-                                       : tc_step(L, update, pooled != nullptr, encode_only);
-  if (s) return s;
-  if ((s = launch_loss_reduce(L, update))) return s;
+  if (L->mpst) {   // model parallel (mp.cu): halo exchange, interior / boundary fields, dX return, loss all-reduce
+    if (encode_only) { set_error("lcae_encode is not available on a model-parallel layer"); return LCAE_ERR_ARG; }
+    for (int ph = 0; ph < 3; ++ph)
+      if ((s = mp_phase(L, ph, update, pooled != nullptr))) return s;
+  } else {
+    s = (L->cfg.precision == LCAE_FP32) ? f32_step(L, update, pooled != nullptr)
+                                         : tc_step(L, update, pooled != nullptr, encode_only);
+    if (s) return s;
+    if ((s = launch_loss_reduce(L, update))) return s;
+    if (update && (s = launch_hwcn_to_nhwc_f32(L, L->dxt, L->dx_nhwc))) return s;
+  }
   if (update) {
-    if ((s = launch_hwcn_to_nhwc_f32(L, L->dxt, L->dx_nhwc))) return s;
-    if (dx && (s = copy_any(L, dx, L->dx_nhwc, (size_t)g.m * g.H * g.W * g.C * 4))) return s;
+    if (dx && (s = copy_any(L, dx, L->dx_nhwc, input_elems(L) * 4))) return s;
     L->steps++;
   }
   if (pooled && (s = copy_any(L, pooled, L->pooled, (size_t)g.m * g.F * (g.k / g.g) * 4))) return s;
@@ -350,8 +406,7 @@ lcae_status lcae_forward(lcae_layer *L, const float *x, float *pooled, double *l
 lcae_status lcae_prefetch_input(lcae_layer *L, const float *x_host) {
   if (!L || !x_host) { set_error("NULL argument"); return LCAE_ERR_ARG; }
   if (is_device_ptr(x_host)) return LCAE_OK;   // nothing to copy
-  const Geo &g = L->geo;
-  const size_t bytes = (size_t)g.m * g.H * g.W * g.C * 4;
+  const size_t bytes = input_elems(L) * 4;
   if (!L->x_pf) {   // first use: the buffer, a copy stream and two events
     LCAE_CK(cudaMalloc(&L->x_pf, bytes));
     LCAE_CK(cudaStreamCreateWithFlags(&L->copy_st, cudaStreamNonBlocking));
@@ -384,6 +439,47 @@ lcae_status lcae_last_loss(lcae_layer *L, double *j_rec, double *j_sparse) {
   LCAE_CK(cudaStreamSynchronize(L->st));
   if (j_rec) *j_rec = L->loss_host[0];
   if (j_sparse) *j_sparse = L->loss_host[1];
+  return LCAE_OK;
+}
+
+lcae_status lcae_mp_phase(lcae_layer *L, int32_t phase, int32_t update, const float *x, float *dx, float *pooled,
+                          double *loss) {
+  if (!L || !L->mpst || !mp_external(L)) {
+    set_error("lcae_mp_phase: needs a model-parallel layer in test mode (world_size > 1, nccl_id == NULL)");
+    return LCAE_ERR_ARG;
+  }
+  if (phase < 0 || phase > 2) { set_error("lcae_mp_phase: phase must be 0, 1 or 2"); return LCAE_ERR_ARG; }
+  lcae_status s;
+  if (phase == 0) {
+    if (!x) { set_error("NULL input"); return LCAE_ERR_ARG; }
+    L->launches = 0;
+    if ((s = stage_input(L, x))) return s;
+  }
+  if ((s = mp_phase(L, phase, update != 0, pooled != nullptr))) return s;
+  if (phase == 2) {
+    if (update) {
+      if (dx && (s = copy_any(L, dx, L->dx_nhwc, input_elems(L) * 4))) return s;
+      L->steps++;
+    }
+    if (pooled && (s = copy_any(L, pooled, L->pooled, (size_t)L->geo.m * L->geo.F * (L->geo.k / L->geo.g) * 4)))
+      return s;
+    if (loss) return read_loss(L, loss);
+    return sync_flags(L);
+  }
+  return LCAE_OK;
+}
+
+lcae_status lcae_mp_buffer(lcae_layer *L, int32_t which, int32_t peer, void **ptr, int64_t *bytes) {
+  if (!L || !L->mpst || which < 0 || which > 3) { set_error("lcae_mp_buffer: bad handle or buffer id"); return LCAE_ERR_ARG; }
+  return mp_buffer(L, which, peer, ptr, bytes);
+}
+
+lcae_status lcae_mp_fields(lcae_layer *L, int32_t *n_interior, int32_t *n_boundary) {
+  if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
+  int a = 0, b = L->geo.F;
+  if (L->mpst) mp_counts(L, &a, &b);
+  if (n_interior) *n_interior = a;
+  if (n_boundary) *n_boundary = b;
   return LCAE_OK;
 }
 

@@ -137,13 +137,17 @@ __global__ void __launch_bounds__(1024) loss_reduce(const double *part, int F, d
   }
 }
 
-// Default init: counter-based uniform rows (unit length), alpha = alpha_init, b = 0, sigma = 1.
-__global__ void __launch_bounds__(256) init_rows(Geo g, int wp, float *W, float *sigma, uint64_t seed) {
+// Default init: counter-based uniform rows (unit length), alpha = alpha_init, b = 0, sigma = 1. Keyed by the GLOBAL
+// field id (row0 + r) * ggc + col0 + c, so a model-parallel tile starts from the untiled layer's weights.
+__global__ void __launch_bounds__(256) init_rows(Geo g, int wp, float *W, float *sigma, uint64_t seed, int row0,
+                                                 int col0, int ggc) {
   __shared__ double sh[32];
   __shared__ float s_sc;
   const int f = blockIdx.x, j = blockIdx.y;
   float *w = W + ((int64_t)f * g.k + j) * wp;
-  uint64_t key = splitmix64(seed ^ 0x5EEDull ^ ((uint64_t)f << 20) ^ (uint64_t)j);
+  const int fr = f / g.gc, fc = f - fr * g.gc;
+  const uint64_t gf = (uint64_t)((row0 + fr) * ggc + col0 + fc);
+  uint64_t key = splitmix64(seed ^ 0x5EEDull ^ (gf << 20) ^ (uint64_t)j);
   double acc = 0.0;
   for (int t = threadIdx.x; t < g.n; t += blockDim.x) {
     float u = (float)((double)(splitmix64(key + t) >> 40) / 16777216.0 - 0.5);
@@ -244,7 +248,8 @@ lcae_status launch_loss_reduce(lcae_layer *L, bool update) {
 
 lcae_status launch_init_params(lcae_layer *L) {
   const Geo &g = L->geo;
-  init_rows<<<dim3(g.F, g.k), 256, 0, L->st>>>(g, L->wp, L->W, L->sigma, L->cfg.seed);
+  init_rows<<<dim3(g.F, g.k), 256, 0, L->st>>>(g, L->wp, L->W, L->sigma, L->cfg.seed, L->cfg.field_row0,
+                                                L->cfg.field_col0, L->cfg.global_grid_c);
   LCAE_CK_LAUNCH(L);
   fill_f32<<<L->sm_count, 256, 0, L->st>>>(L->alpha, g.F, L->cfg.alpha_init);
   LCAE_CK_LAUNCH(L);

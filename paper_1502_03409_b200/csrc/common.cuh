@@ -50,6 +50,14 @@ struct F32Scratch {
 };
 
 struct TcScratch;   // bf16 tensor-core path (tc_path.cu)
+struct MpState;     // model-parallel tile state (mp.cu)
+
+// One rank's tile of a model-parallel layer (mp.cu): field rows [R0, R1) x cols [C0, C1) of the global grid;
+// need / own = pixel rectangles (y0, y1, x0, x1) read by its fields / owned (input and input gradient).
+struct MpTile {
+  int tr_n = 1, tc_n = 1, R0 = 0, R1 = 0, C0 = 0, C1 = 0;
+  int need[4] = {0, 0, 0, 0}, own[4] = {0, 0, 0, 0};
+};
 
 }  // namespace lcae
 
@@ -93,6 +101,7 @@ struct lcae_layer {
   int launches = 0;
   lcae::F32Scratch f32;
   lcae::TcScratch *tc = nullptr;
+  lcae::MpState *mpst = nullptr;   // model-parallel state (world_size > 1)
   // profiling (lcae_profile): events around the dominant kernel
   int prof_on = 0, prof_n = 0;
   cudaEvent_t *prof_ev = nullptr;   // [2 * 4096]
@@ -139,7 +148,23 @@ lcae_status f32_step(lcae_layer *L, bool update, bool want_pooled);
 
 lcae_status tc_alloc(lcae_layer *L);
 void tc_free(lcae_layer *L);
-lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_only = false);
+// flist/nfl: the fields of this launch (NULL: all); first: zero the dX accumulator; last: run the finalize kernel;
+// reserve_clusters: SM pairs left free (model-parallel interior launch overlapping the NCCL halo exchange)
+lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_only = false, const int *flist = nullptr,
+                    int nfl = 0, bool first = true, bool last = true, int reserve_clusters = 0);
+lcae_status tc_finalize(lcae_layer *L);
+
+// model parallelism (mp.cu)
+lcae_status mp_tile(const lcae_config *c, const Geo &global, int rank, MpTile *t);
+lcae_status mp_init(lcae_layer *L, const Geo &global);
+void mp_free(lcae_layer *L);
+size_t mp_input_elems(lcae_layer *L);
+lcae_status mp_stage(lcae_layer *L, const float *x_dev);
+lcae_status mp_phase(lcae_layer *L, int phase, bool update, bool want_pooled);
+bool mp_external(lcae_layer *L);
+lcae_status mp_buffer(lcae_layer *L, int which, int peer, void **ptr, int64_t *bytes);
+void mp_counts(lcae_layer *L, int *n_int, int *n_bnd);
+const MpTile &mp_tile_of(lcae_layer *L);
 double *tc_loss_part(lcae_layer *L);
 int tc_loss_count(lcae_layer *L);
 

@@ -147,6 +147,14 @@ __device__ __forceinline__ void red_v4_if(float *p, float a, float b, float c, f
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t@p red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
       "f"(a), "f"(b), "f"(c), "f"(d), "r"((int)pred));
 }
+// TMA tensor reduce-add: the box at (c0, c1) of the fp32 tensor += the smem box at src (bulk_group completion;
+// the L2 performs the element-wise adds atomically). src: SWIZZLE_NONE box image, rows of box-dim-0 floats.
+__device__ __forceinline__ void tma_red_add_2d(const CUtensorMap *m, const void *src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
 // Invalidate one 128-byte L2 line without writing it back (dead scratch data).
 __device__ __forceinline__ void discard_l2(const void *p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");

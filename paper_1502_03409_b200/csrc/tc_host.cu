@@ -112,8 +112,31 @@ struct TcScratch {
   uint8_t *dscr = nullptr;
   CUtensorMap tmW;
   CUtensorMap tmX[tc::NXMAP];
-  uint32_t *xpieces = nullptr;
+  CUtensorMap tmD[tc::NDMAP];
+  uint32_t *xpieces = nullptr, *dxpieces = nullptr;
 };
+
+// Pieces of the patch rows [r0, r0 + rows) of a field window: runs of consecutive image rows (one per receptive-field
+// row) split into power-of-two boxes of at most 2^maxlg rows. Word: offset in the window (16 b) | first row relative
+// to r0 (8 b) << 16 | log2 height (8 b) << 24. Returns false if more than cap pieces are needed.
+static bool window_pieces(const Geo &g, int r0, int rows, int maxlg, int cap, uint32_t *out) {
+  int np = 0, r = 0;
+  while (r < rows) {
+    const int nn = r0 + r, ry = nn / g.RW;
+    const int run = std::min(rows - r, (ry + 1) * g.RW - nn);
+    int off = ry * g.W * g.C + (nn - ry * g.RW), left = run;
+    while (left > 0) {
+      int lg = maxlg;
+      while ((1 << lg) > left) --lg;
+      if (np >= cap) return false;
+      out[np++] = (uint32_t)off | ((uint32_t)r << 16) | ((uint32_t)lg << 24);
+      off += 1 << lg;
+      r += 1 << lg;
+      left -= 1 << lg;
+    }
+  }
+  return true;
+}
 
 lcae_status tc_alloc(lcae_layer *L) {
   const Geo &g = L->geo;
@@ -157,24 +180,28 @@ lcae_status tc_alloc(lcae_layer *L) {
     }
   // per-tile pieces: runs of consecutive image rows (one per receptive-field row) split into 2^i-row boxes
   std::vector<uint32_t> pcs((size_t)T * tc::XPMAX, 0xFFFFFFFFu);
-  for (int j = 0; j < T; ++j) {
-    int np = 0, r = 0;
-    const int rows = std::min(tc::NT, g.n - j * tc::NT);
-    while (r < rows) {
-      const int nn = j * tc::NT + r, ry = nn / g.RW;
-      const int run = std::min(rows - r, (ry + 1) * g.RW - nn);
-      int off = ry * g.W * g.C + (nn - ry * g.RW), left = run;
-      while (left > 0) {
-        int lg = 6;
-        while ((1 << lg) > left) --lg;
-        if (np >= tc::XPMAX) { set_error("bf16 path: too many X pieces per tile (rf_w*C too small)"); return LCAE_ERR_CONFIG; }
-        pcs[(size_t)j * tc::XPMAX + np++] = (uint32_t)off | ((uint32_t)r << 16) | ((uint32_t)lg << 24);
-        off += 1 << lg;
-        r += 1 << lg;
-        left -= 1 << lg;
+  for (int j = 0; j < T; ++j)
+    if (!window_pieces(g, j * tc::NT, std::min(tc::NT, g.n - j * tc::NT), 6, tc::XPMAX, &pcs[(size_t)j * tc::XPMAX])) {
+      set_error("bf16 path: too many X pieces per tile (rf_w*C too small)");
+      return LCAE_ERR_CONFIG;
+    }
+  // dX reduce pieces per 16-column chunk of every tile (box heights <= 16)
+  std::vector<uint32_t> dpc((size_t)T * 4 * tc::DXPMAX, 0xFFFFFFFFu);
+  for (int j = 0; j < T; ++j)
+    for (int q = 0; q < 4; ++q) {
+      const int r0 = j * tc::NT + 16 * q, rows = std::min(16, g.n - r0);
+      if (rows > 0 && !window_pieces(g, r0, rows, 4, tc::DXPMAX, &dpc[((size_t)j * 4 + q) * tc::DXPMAX])) {
+        set_error("bf16 path: too many dX pieces per 16-row chunk");
+        return LCAE_ERR_CONFIG;
       }
     }
-  }
+  LCAE_CK(cudaMalloc(&s->dxpieces, dpc.size() * 4));
+  LCAE_CK(cudaMemcpy(s->dxpieces, dpc.data(), dpc.size() * 4, cudaMemcpyHostToDevice));
+  for (int i = 0; i < tc::NDMAP; ++i)
+    if (!make_tmap_2d_f32(&s->tmD[i], L->dxt, prow, (uint64_t)L->mp, (uint64_t)L->mp, 1u << i, 32)) {
+      set_error("cuTensorMapEncodeTiled failed for dX");
+      return LCAE_ERR_CUDA;
+    }
   LCAE_CK(cudaMalloc(&s->xpieces, pcs.size() * 4));
   LCAE_CK(cudaMemcpy(s->xpieces, pcs.data(), pcs.size() * 4, cudaMemcpyHostToDevice));
   return LCAE_OK;
@@ -183,19 +210,22 @@ lcae_status tc_alloc(lcae_layer *L) {
 void tc_free(lcae_layer *L) {
   if (!L->tc) return;
   TcScratch *s = L->tc;
-  for (void *p : {(void *)s->loss_part, (void *)s->da_part, (void *)s->db_part, (void *)s->rowsq_part, (void *)s->trace, (void *)s->xpieces, (void *)s->dbscr, (void *)s->dscr})
+  for (void *p : {(void *)s->loss_part, (void *)s->da_part, (void *)s->db_part, (void *)s->rowsq_part, (void *)s->trace, (void *)s->xpieces, (void *)s->dxpieces, (void *)s->dbscr, (void *)s->dscr})
     if (p) cudaFree(p);
   delete s;
   L->tc = nullptr;
 }
 
-lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_only) {
+lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_only, const int *flist, int nfl,
+                    bool first, bool last, int reserve_clusters) {
   const Geo &g = L->geo;
   TcScratch *s = L->tc;
   tc::Params P;
   P.tmW = s->tmW;
   for (int i = 0; i < tc::NXMAP; ++i) P.tmX[i] = s->tmX[i];
   P.xpieces = s->xpieces;
+  for (int i = 0; i < tc::NDMAP; ++i) P.tmD[i] = s->tmD[i];
+  P.dxpieces = s->dxpieces;
   P.g = g;
   P.T = s->T;
   P.mp = L->mp;
@@ -227,10 +257,16 @@ lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_on
   P.dscr = s->dscr;
   P.gW = L->gW;
   P.flags = L->flags_dev;
+  P.flist = flist;
+  P.nfl = nfl;
   P.trace = s->trace_on ? s->trace : nullptr;
-  if (update) LCAE_CK(cudaMemsetAsync(L->dxt, 0, (size_t)g.H * g.W * g.C * L->mp * 4, L->st));
+  if (update && first) LCAE_CK(cudaMemsetAsync(L->dxt, 0, (size_t)g.H * g.W * g.C * L->mp * 4, L->st));
+  if (flist && nfl == 0) return update && last ? tc_finalize(L) : LCAE_OK;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(s->grid);
+  // a model-parallel interior launch leaves `reserve_clusters` SM pairs free for the NCCL halo kernels
+  const int ncl_all = s->grid / s->CB;
+  const int ncl_use = std::max(1, std::min(ncl_all - reserve_clusters, flist ? nfl : g.F));
+  cfg.gridDim = dim3(ncl_use * s->CB);
   cfg.blockDim = dim3(tc::NTHREADS);
   cfg.dynamicSmemBytes = s->smem;
   cfg.stream = L->st;
@@ -261,7 +297,14 @@ lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_on
   LCAE_CK(cudaLaunchKernelEx(&cfg, kern, P));
   LCAE_CK_LAUNCH(L);
   if (prof) LCAE_CK(cudaEventRecord(L->prof_ev[2 * L->prof_n++ + 1], L->st));
-  if (update) {
+  if (update && last) return tc_finalize(L);
+  return LCAE_OK;
+}
+
+lcae_status tc_finalize(lcae_layer *L) {
+  const Geo &g = L->geo;
+  TcScratch *s = L->tc;
+  {
     tc::finalize_kernel<<<g.F, 128, 0, L->st>>>(
         g, s->CB, L->n_al, s->da_part, s->db_part, s->rowsq_part, L->alpha, L->b, L->sigma, L->W, L->Wb, L->va,
         L->vb, L->cfg.lr, L->cfg.momentum, L->cfg.alpha_min, L->cfg.keep_grads ? L->galpha : nullptr,

@@ -52,11 +52,17 @@ constexpr int MAX_NPAD = 1024;
 
 constexpr int NXMAP = 7;       // X tensor maps with box heights 1, 2, 4, ..., 64 rows
 constexpr int XPMAX = 64;      // max TMA pieces per 64-row X tile
+constexpr int NDMAP = 5;       // dX reduce tensor maps with box heights 1, 2, 4, 8, 16 rows (x 32 samples)
+constexpr int DXPMAX = 16;     // max TMA pieces per 16-column dX chunk
 
 struct Params {
   CUtensorMap tmW;   // W~ bf16 [F*KP][n_al], box (64, 128)
   CUtensorMap tmX[NXMAP];   // X HWCN bf16 viewed as [H*W*C rows][mp], box (64 samples, 2^i rows)
   const uint32_t *xpieces;  // [T][XPMAX]: off (16 b) | dst row (8 b) << 16 | log2 rows (8 b) << 24; 0xFFFFFFFF ends
+  CUtensorMap tmD[NDMAP];   // dX HWCN f32 viewed as [H*W*C rows][mp], box (32 samples, 2^i rows), no swizzle
+  const uint32_t *dxpieces; // [T][4][DXPMAX]: the pieces of 16-column chunk q of tile j, same encoding
+  const int *flist;         // nullable: the launch walks fields flist[0..nfl) (model-parallel interior / boundary
+  int nfl;                  // split); NULL: fields 0..F-1
   Geo g;
   int T, mp, CB, n_al, wp, mode, want_pooled, keep_grads;
   int dbg;   // dev-only (LCAE_DEBUG_FLAGS): bit 0 skips the dX reductions, bit 1 the W~/shadow stores,
@@ -87,9 +93,9 @@ struct __align__(1024) Smem {
   uint8_t Dl[2][16384];      // pass 0: X slots 2,3
   uint8_t negI[8192];        // -I (64 x 64 bf16, SW128)
   float recv[2][128][16];    // peer's dW partial for this CTA's owned 16-column chunks, [half][row][col]
-  float stg[NEPI][32][16];   // per-warp transpose staging of the own dW chunk (16-byte chunks swizzled);
+  float stg[NEPI][32][16];   // per-warp 2 KB staging: the own dW chunk's transpose (16-byte chunks swizzled), then
+                             // the dX rounds ([16 patch rows][32 samples], the TMA reduce-add source);
                              // forward / encode modes: recv + stg (contiguous) = 8 x 4 KB pooled-output staging
-  uint16_t off[MAX_NPAD];    // pixel-feature offset of patch row n inside the field window (host-checked < 2^16)
   float bs[MAX_NPAD];        // b_f of the current field (epilogue)
   float sig[KP];
   float isig[KP];            // 1 / sig
@@ -187,6 +193,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
   // a flagged error (this step's input had a non-finite value, or an earlier loss was non-finite) freezes the
   // parameters: every CTA reads the same flags (written by earlier kernels), so all return together
   if (step && (P.flags[0] | P.flags[1])) return;
+  const int nfl = P.flist ? P.nfl : P.g.F;
+  auto fid = [&](int i) { return P.flist ? __ldg(P.flist + i) : i; };
   // trace: lane 0 of the producers / MMA warp and of epilogue warp 2 record their barrier-wait cycles
   const bool trec = TR && P.trace != nullptr && lane == 0 && (warp <= 2 || warp == XWARP);
   const long long t_start = clock64();
@@ -212,10 +220,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       tmark = t_;                                                                                \
     }                                                                                            \
   } while (0)
-  for (int t = threadIdx.x; t < T * NT; t += NTHREADS) {
-    int ry = t / g.RW, rem = t - ry * g.RW;
-    S.off[t] = (uint16_t)(t < n ? ry * g.W * g.C + rem : 0);
-  }
   {  // X slots start zeroed: rows past n of the last tile are never written (their products are masked,
      // but must stay finite)
     uint4 *z = reinterpret_cast<uint4 *>(S.Xr[0]);
@@ -265,7 +269,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       const uint64_t pol = ptx::policy_evict_first();   // W is streamed once per pass: keep X / dX in L2
       uint32_t q = 0;
       const int npass = step ? 3 : (enc ? 1 : 2);
-      for (int f = cid; f < g.F; f += ncl)
+      for (int fi = cid; fi < nfl; fi += ncl) {
+        const int f = fid(fi);
         for (int pass = 0; pass < npass; ++pass)
           for (int j = 0; j < T; ++j, ++q) {
             const int s = q % NW;
@@ -276,11 +281,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             else
               ptx::tma_load_2d(S.Wr[s], &P.tmW, &S.wfull[s], j * NT, f * KP);
           }
+      }
     } else if (lane == 1 && step) {
       // =================================================================== delta store-out (bulk S2G)
       // every pass-1 delta tile goes to this CTA's global scratch as its swizzled smem image; pass 2 reloads it
       uint32_t ud = 0, nf = 0;
-      for (int f = cid; f < g.F; f += ncl, ++nf) {
+      for (int fi = cid; fi < nfl; fi += ncl, ++nf) {
         uint8_t *dst = P.dscr + (size_t)blockIdx.x * T * 16384;
         for (int j = 0; j < T; ++j, ++ud) {
           const uint32_t db_ = ud & 1;
@@ -303,7 +309,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
 #pragma unroll
       for (int i = 0; i < NXMAP; ++i) ptx::tma_prefetch(&P.tmX[i]);
     }
-    for (int f = cid; f < g.F; f += ncl, ++nf) {
+    for (int fi = cid; fi < nfl; fi += ncl, ++nf) {
+      const int f = fid(fi);
       const int fr = f / g.gc, fc = f - fr * g.gc;
       const int pixbase = (fr * g.s * g.W + fc * g.s) * g.C;
       // X_j = runs of consecutive image rows (one per receptive-field row): a few TMA boxes per 64-sample half;
@@ -414,7 +421,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           UMMA_E(tb + dcol, ad, bd, id_nx, 1);
         }
       };
-      for (int f = cid; f < g.F; f += ncl, ++nf) {
+      for (int fi = cid; fi < nfl; fi += ncl, ++nf) {
         // ---- pass 0: U^T = X^T W~^T (encode-only: into one of 4 U buffers, so that the next fields' encodes
         // overlap this field's pooling epilogue)
         const uint32_t ucol = enc ? 128 * (nf & 3) : 384;
@@ -545,7 +552,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     const uint32_t peer_recv = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.recv[half][row][0]), crank ^ 1u) : 0u;
     const uint32_t peer_recv_full = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.recv_full), crank ^ 1u) : 0u;
     const uint32_t peer_free_bar = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.peer_free), crank ^ 1u) : 0u;
-    for (int f = cid; f < g.F; f += ncl, ++nf) {
+    for (int fi = cid; fi < nfl; fi += ncl, ++nf) {
+      const int f = fid(fi);
       const int fr = f / g.gc, fc = f - fr * g.gc;
       const int64_t pixbase = ((int64_t)fr * g.s * g.W + (int64_t)fc * g.s) * g.C;
       ptx::named_bar_sync(1, 32 * NEPI);
@@ -731,8 +739,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         // per-field invariants of this thread's E2 work, hoisted out of the tile loop
         const bool do_red = !FULL || !(P.dbg & 1), do_sgd = !FULL || !(P.dbg & 2);
         const bool has_v = FULL && P.vW != nullptr, keep = FULL && P.keep_grads != 0;
-        float *const dxcol = P.dxt + pixbase * mp + (s0 + qd * 32 + (lane & ~3));   // dX band of this lane group
-        const bool grp_ok = s0 + qd * 32 + (lane & ~3) < mp;
         const float *wrp[4];
         float sgr[4], isgr[4];
         bool rok[4];
@@ -753,25 +759,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           const int swr = (lane >> 1) & 3;                     // swizzle of this lane's row (row = lane)
           float *stg = &S.stg[ew][0][0];                       // [32 rows][16] fp32, 16-byte chunks swizzled
           const float *rcv = &S.recv[half][qd * 32][0];        // same layout, written by the peer
-          // dx = alpha W^T D - delta (both halves accumulated in TMEM), overlap-added into the image gradient with
-          // 16-byte reductions: 4x4 lane transposes give each lane 4 consecutive samples of one column.
-          auto dx_reduce = [&](const float (&xv)[32]) {
-            const int r4 = lane & 3;
-            const bool o1 = r4 & 1, o2 = r4 & 2;
-            const bool full = (j + 1) * NT <= n;   // all but the ragged last tile
+          // dx = alpha W^T D - delta (both halves accumulated in TMEM) is overlap-added into the image gradient by the
+          // TMA unit: each 16-column round is staged in this warp's slice as [16 patch rows][32 samples] (one
+          // conflict-free 128-byte row per column) and reduce-added (cp.reduce.async.bulk.tensor .add.f32) in boxes
+          // of consecutive image rows from the host piece table (lanes 0..15 issue one piece each).
+          const uint32_t *dxp = P.dxpieces + ((size_t)j * 4 + 2 * half) * DXPMAX;
+          const uint32_t pw0 = lane < DXPMAX ? __ldg(dxp + lane) : 0xFFFFFFFFu;
+          const uint32_t pw1 = lane < DXPMAX ? __ldg(dxp + DXPMAX + lane) : 0xFFFFFFFFu;
+          float xv[32];
+          auto dx_round = [&](auto RI, uint32_t pw) {
+            constexpr int r = decltype(RI)::value;
+            ptx::bulk_wait_read0();   // this lane's earlier reduce boxes have read the staging slice
+            __syncwarp();
 #pragma unroll
-            for (int blk = 0; blk < 8; ++blk) {
-              float a0 = xv[4 * blk], a1 = xv[4 * blk + 1], a2 = xv[4 * blk + 2], a3 = xv[4 * blk + 3];
-              float t0 = __shfl_xor_sync(0xffffffffu, o1 ? a0 : a1, 1);
-              float t1 = __shfl_xor_sync(0xffffffffu, o1 ? a2 : a3, 1);
-              if (o1) { a0 = t0; a2 = t1; } else { a1 = t0; a3 = t1; }
-              t0 = __shfl_xor_sync(0xffffffffu, o2 ? a0 : a2, 2);
-              t1 = __shfl_xor_sync(0xffffffffu, o2 ? a1 : a3, 2);
-              if (o2) { a0 = t0; a1 = t1; } else { a2 = t0; a3 = t1; }
-              const int nn = j * NT + hc + 4 * blk + r4;
-              ptx::red_v4_if(dxcol + (uint32_t)S.off[nn] * (uint32_t)mp, a0, a1, a2, a3,
-                             (full || nn < n) && grp_ok && do_red);
-            }
+            for (int c = 0; c < 16; ++c) stg[c * 32 + lane] = xv[16 * r + c];
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (pw != 0xFFFFFFFFu && do_red)
+              ptx::tma_red_add_2d(&P.tmD[pw >> 24], stg + ((pw >> 16) & 0xFFu) * 32, s0 + qd * 32,
+                                  (int)pixbase + (int)(pw & 0xFFFFu));
+            ptx::bulk_commit();
           };
           // dW_j (lanes = filter rows, this warp's 32 columns). CTA c owns the 16-column chunk [16c, 16c+16) of
           // each half; the batch slices of that chunk are summed over the cluster (DSMEM), then the projected SGD
@@ -799,9 +806,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             }
           }
           float4 dq[4 * NCH];   // summed dW chunk(s), coalesced layout
+          ptx::bulk_wait_read0();   // the previous tile's last dX round has been read out of the staging slice
+          __syncwarp();
           if constexpr (CB > 1) {
             // the dW half the peer owns goes out first and the own half is staged, so that the exchange is in
-            // flight while this warp reduces dX
+            // flight while this warp stages and issues the dX reductions
             {
               float dw[32];   // dw[0..15] = the owned chunk, dw[16..31] = the peer's chunk
               ptx::tmem_ld16(tl + base + 64 + hc + 16 * crank, dw);
@@ -821,24 +830,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
                     make_float4(dw[4 * t], dw[4 * t + 1], dw[4 * t + 2], dw[4 * t + 3]);
             }
             TMARK(40);
-            {
-              float xv[32];
-              ptx::tmem_ld16(tl + base + hc, xv);
-              ptx::tmem_ld16(tl + base + hc + 16, xv + 16);
-              ptx::tmem_ld_wait();
-              ptx::tc_fence_before();
-              __syncwarp();
-              if (lane == 0) ptx::mbar_arrive(&S.p2_empty[pb]);   // TMEM buffer pb fully read by this warp
-              dx_reduce(xv);
-            }
-            TMARK(36);
+            ptx::tmem_ld16(tl + base + hc, xv);
+            ptx::tmem_ld16(tl + base + hc + 16, xv + 16);
+            ptx::tmem_ld_wait();
+            ptx::tc_fence_before();
             __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&S.p2_empty[pb]);   // TMEM buffer pb fully read by this warp
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const int r = 8 * i + rr, o = r * 16 + 4 * (cq ^ ((r >> 1) & 3));
               dq[i] = *reinterpret_cast<const float4 *>(stg + o);
             }
-            __syncwarp();
+            dx_round(std::integral_constant<int, 0>{}, pw0);   // first dX round while the peer's chunk arrives
+            TMARK(36);
             TMARK(41);
             // + the peer's batch slice, read straight from the receive slice in the same layout
             TWAIT(22, ptx::mbar_wait(&S.recv_full, u2 & 1));
@@ -852,14 +856,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             if (lane == 0)   // receive slice read: the peer may send the next tile (reads only; relaxed suffices)
               ptx::mbar_arrive_remote_relaxed(peer_free_bar);
           } else {
-            {
-              float xv[32];
-              ptx::tmem_ld16(tl + base + hc, xv);
-              ptx::tmem_ld16(tl + base + hc + 16, xv + 16);
-              ptx::tmem_ld_wait();
-              dx_reduce(xv);
-            }
-            TMARK(36);
+            ptx::tmem_ld16(tl + base + hc, xv);
+            ptx::tmem_ld16(tl + base + hc + 16, xv + 16);
             float dw[32];
             ptx::tmem_ld16(tl + base + 64 + hc, dw);
             ptx::tmem_ld16(tl + base + 64 + hc + 16, dw + 16);
@@ -884,6 +882,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               }
               __syncwarp();
             }
+            dx_round(std::integral_constant<int, 0>{}, pw0);
+            TMARK(36);
           }
           TMARK(42);
           if (do_sgd) {
@@ -927,6 +927,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               }
             }
           }
+          dx_round(std::integral_constant<int, 1>{}, pw1);   // second dX round (its staging read overlaps the next tile)
           TMARK(37);
         }
       }
@@ -964,6 +965,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     }
   }
   // ---- teardown
+  if (step && warp >= 2 && warp < XWARP) ptx::bulk_wait0();   // every dX reduce box complete before exit
   if (trec) atomicAdd(&S.tr[warp == 1 ? 10 : warp == 0 ? 25 : warp == XWARP ? 24 : 26],
                       (unsigned long long)(clock64() - t_start));
   ptx::tc_fence_before();

@@ -35,4 +35,20 @@ inline bool make_tmap_2d_bf16(CUtensorMap *m, const void *base, uint64_t rows, u
   return r == CUDA_SUCCESS;
 }
 
+// 2D fp32 tensor [rows][cols] with row pitch `pitch_elems`; box = (box_cols, box_rows), no swizzle (the reduce-add
+// target of the dX staging: rows of box_cols consecutive samples).
+inline bool make_tmap_2d_f32(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols, uint64_t pitch_elems,
+                             uint32_t box_rows, uint32_t box_cols) {
+  auto fn = tma_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_elems * 4};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace lcae

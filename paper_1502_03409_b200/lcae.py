@@ -33,6 +33,8 @@ class Config(C.Structure):
         ("seed", C.c_uint64),
         ("precision", C.c_int32), ("keep_grads", C.c_int32),
         ("field_row0", C.c_int32), ("field_col0", C.c_int32), ("global_grid_c", C.c_int32),
+        ("world_size", C.c_int32), ("rank", C.c_int32), ("tiles_r", C.c_int32), ("tiles_c", C.c_int32),
+        ("nccl_id", C.c_void_p),
         ("stream", C.c_void_p),
     ]
 
@@ -44,7 +46,12 @@ def _load():
     P = C.c_void_p
     sigs = {
         "lcae_config_default": (None, [C.POINTER(Config)]),
-        "lcae_geometry": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+        "lcae_geometry": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+        "lcae_nccl_unique_id": (C.c_int, [P]),
+        "lcae_mp_phase": (C.c_int, [P, C.c_int32, C.c_int32, P, P, P, C.POINTER(C.c_double)]),
+        "lcae_mp_buffer": (C.c_int, [P, C.c_int32, C.c_int32, C.POINTER(P), C.POINTER(C.c_int64)]),
+        "lcae_mp_fields": (C.c_int, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "lcae_create": (C.c_int, [C.POINTER(Config), C.POINTER(P)]),
         "lcae_destroy": (C.c_int, [P]),
         "lcae_set_params": (C.c_int, [P, P, P, P]),
@@ -88,7 +95,8 @@ lib = _load()
 # Every symbol include/lcae.h declares (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("lcae_config_default", "lcae_geometry", "lcae_create", "lcae_destroy", "lcae_set_params",
                "lcae_get_params", "lcae_get_grads", "lcae_forward", "lcae_encode", "lcae_step", "lcae_last_loss",
-               "lcae_sync", "lcae_field_losses",
+               "lcae_sync", "lcae_field_losses", "lcae_nccl_unique_id", "lcae_mp_phase", "lcae_mp_buffer",
+               "lcae_mp_fields",
                "lcae_topk_init", "lcae_topk_update", "lcae_lcn", "lcae_prefetch_input",
                "lcae_dx_device", "lcae_counters", "lcae_region_add", "lcae_last_launch_count",
                "lcae_profile", "lcae_profile_read",
@@ -112,7 +120,8 @@ def _ptr(a) -> Optional[int]:
 
 
 def make_config(shape, precision=BF16, keep_grads=False, stream=None, seed=0, field_row0=0, field_col0=0,
-                global_grid_c=0, img_h=None, img_w=None) -> Config:
+                global_grid_c=0, img_h=None, img_w=None, world_size=1, rank=0, tiles=(0, 0), nccl_id=None) -> Config:
+    """nccl_id: a 128-byte bytes object from nccl_unique_id() (kept alive by the returned Config)."""
     cfg = Config()
     lib.lcae_config_default(C.byref(cfg))
     cfg.img_h = shape.img_h if img_h is None else img_h
@@ -126,14 +135,35 @@ def make_config(shape, precision=BF16, keep_grads=False, stream=None, seed=0, fi
     cfg.precision = precision
     cfg.keep_grads = int(bool(keep_grads))
     cfg.field_row0, cfg.field_col0, cfg.global_grid_c = field_row0, field_col0, global_grid_c
+    cfg.world_size, cfg.rank = world_size, rank
+    cfg.tiles_r, cfg.tiles_c = tiles
+    if nccl_id is not None:
+        buf = C.create_string_buffer(bytes(nccl_id), 128)
+        cfg._nccl_buf = buf   # keep alive with the config
+        cfg.nccl_id = C.cast(buf, C.c_void_p)
     cfg.stream = stream
     return cfg
 
 
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for Config.nccl_id (lcae_nccl_unique_id; one rank creates, all use)."""
+    buf = C.create_string_buffer(128)
+    check(lib.lcae_nccl_unique_id(buf))
+    return buf.raw
+
+
 def geometry(cfg: Config):
     gr, gc, npar = C.c_int32(), C.c_int32(), C.c_int64()
-    check(lib.lcae_geometry(C.byref(cfg), C.byref(gr), C.byref(gc), C.byref(npar)))
+    check(lib.lcae_geometry(C.byref(cfg), C.byref(gr), C.byref(gc), C.byref(npar), None, None))
     return gr.value, gc.value, npar.value
+
+
+def tile_geometry(cfg: Config):
+    """(grid_r, grid_c, n_params, own_px (y0, y1, x0, x1), own_fields (R0, R1, C0, C1)) of this rank."""
+    gr, gc, npar = C.c_int32(), C.c_int32(), C.c_int64()
+    px, fl = (C.c_int32 * 4)(), (C.c_int32 * 4)()
+    check(lib.lcae_geometry(C.byref(cfg), C.byref(gr), C.byref(gc), C.byref(npar), px, fl))
+    return gr.value, gc.value, npar.value, tuple(px), tuple(fl)
 
 
 class Layer:
@@ -147,6 +177,10 @@ class Layer:
         self.n = cfg.rf_h * cfg.rf_w * cfg.img_c
         self.m = cfg.batch
         self.img_shape = (cfg.batch, cfg.img_h, cfg.img_w, cfg.img_c)
+        if cfg.world_size > 1:   # model parallel: x / dx are this rank's owned pixels
+            _, _, _, self.own_px, self.own_fields = tile_geometry(cfg)
+            y0, y1, x0, x1 = self.own_px
+            self.img_shape = (cfg.batch, y1 - y0, x1 - x0, cfg.img_c)
         h = C.c_void_p()
         check(lib.lcae_create(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -194,6 +228,24 @@ class Layer:
     def last_loss(self):
         a, b = C.c_double(), C.c_double()
         check(lib.lcae_last_loss(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def mp_phase(self, phase, update=True, x=None, dx=None, pooled=None, want_loss=False):
+        """Model-parallel test mode: one of the three phases of a step (include/lcae.h lcae_mp_phase)."""
+        loss = C.c_double(0.0)
+        check(lib.lcae_mp_phase(self.h, phase, int(bool(update)), _ptr(x), _ptr(dx), _ptr(pooled),
+                                C.byref(loss) if want_loss else None))
+        return loss.value if want_loss else None
+
+    def mp_buffer(self, which, peer):
+        """(device pointer, bytes) of exchange buffer `which` (0 halo send, 1 halo recv, 2 dX send, 3 dX recv)."""
+        p, n = C.c_void_p(), C.c_int64()
+        check(lib.lcae_mp_buffer(self.h, which, peer, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def mp_fields(self):
+        a, b = C.c_int32(), C.c_int32()
+        check(lib.lcae_mp_fields(self.h, C.byref(a), C.byref(b)))
         return a.value, b.value
 
     def sync(self):

