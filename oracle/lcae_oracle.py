@@ -120,8 +120,9 @@ def rica_field(W_f, alpha_f, b_f, x_f, lam, eps, g):
     dalpha = float((dh * U).sum())                               # h = alpha U
     db = delta.sum(axis=0)                                       # SPEC.md:104 db = sum_i 2(recon_i - x_i)
     dx = a * (dh @ W) - delta                                    # R11 total derivative
+    # dalpha_abs = sum |dh (.) U|: the scale of the rounding error of the sum dalpha (R22)
     return dict(J_rec=float(J_rec), J_sparse=float(J_sparse), p=s, h=h, U=U,
-                dW=dW, dalpha=dalpha, db=db, dx=dx)
+                dW=dW, dalpha=dalpha, db=db, dx=dx, dalpha_abs=float(np.abs(dh * U).sum()))
 
 
 def rica_objective(W_f, alpha_f, b_f, x_f, lam, eps, g=1):

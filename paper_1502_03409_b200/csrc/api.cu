@@ -224,6 +224,8 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
   if ((s = local_geo(cfg, gg, &tile, &g))) return s;
   lcae_layer *L = new lcae_layer();
   L->cfg = *cfg;
+  L->poison = getenv("LCAE_DEV_POISON") ? atoi(getenv("LCAE_DEV_POISON")) : 0;
+  L->canary = getenv("LCAE_DEV_CANARY") ? atoi(getenv("LCAE_DEV_CANARY")) : 0;
   if (L->cfg.world_size > 1) {   // the tile's global field offsets key the counter-based init / reinit
     L->cfg.field_row0 = tile.R0;
     L->cfg.field_col0 = tile.C0;
@@ -252,50 +254,50 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
   L->n_al = (int)((n + 7) / 8 * 8);
   L->wp = cfg->precision == LCAE_FP32 ? (int)n : L->n_al;   // fp32 master row pitch (16-byte rows, bf16)
   const size_t wp = L->wp;
-  CKF(cudaMalloc(&L->W, F * k * wp * 4));
+  CKF(dmalloc(L, &L->W, F * k * wp * 4));
   CKF(cudaMemsetAsync(L->W, 0, F * k * wp * 4, L->st));
-  CKF(cudaMalloc(&L->sigma, F * k * 4));
-  CKF(cudaMalloc(&L->alpha, F * 4));
-  CKF(cudaMalloc(&L->b, F * n * 4));
+  CKF(dmalloc(L, &L->sigma, F * k * 4));
+  CKF(dmalloc(L, &L->alpha, F * 4));
+  CKF(dmalloc(L, &L->b, F * n * 4));
   if (cfg->momentum > 0.f) {
-    CKF(cudaMalloc(&L->vW, F * k * wp * 4));
-    CKF(cudaMalloc(&L->va, F * 4));
-    CKF(cudaMalloc(&L->vb, F * n * 4));
+    CKF(dmalloc(L, &L->vW, F * k * wp * 4));
+    CKF(dmalloc(L, &L->va, F * 4));
+    CKF(dmalloc(L, &L->vb, F * n * 4));
     CKF(cudaMemsetAsync(L->vW, 0, F * k * wp * 4, L->st));
     CKF(cudaMemsetAsync(L->va, 0, F * 4, L->st));
     CKF(cudaMemsetAsync(L->vb, 0, F * n * 4, L->st));
   }
   L->mp = cfg->precision == LCAE_FP32 ? g.m : (g.m + 7) / 8 * 8;
   const size_t mp = L->mp;
-  CKF(cudaMalloc(&L->x_stage, m * img * 4));   // >= the owned pixels of a model-parallel rank
-  CKF(cudaMalloc(&L->dxt, mp * img * 4));
-  CKF(cudaMalloc(&L->dx_nhwc, m * img * 4));
-  CKF(cudaMalloc(&L->pooled, m * F * (k / g.g) * 4));
-  CKF(cudaMalloc(&L->loss_part, F * 2 * sizeof(double)));
-  CKF(cudaMalloc(&L->loss_dev, 2 * sizeof(double)));
+  CKF(dmalloc(L, &L->x_stage, m * img * 4));   // >= the owned pixels of a model-parallel rank
+  CKF(dmalloc(L, &L->dxt, mp * img * 4));
+  CKF(dmalloc(L, &L->dx_nhwc, m * img * 4));
+  CKF(dmalloc(L, &L->pooled, m * F * (k / g.g) * 4));
+  CKF(dmalloc(L, &L->loss_part, F * 2 * sizeof(double)));
+  CKF(dmalloc(L, &L->loss_dev, 2 * sizeof(double)));
   CKF(cudaMemsetAsync(L->loss_dev, 0, 2 * sizeof(double), L->st));
-  CKF(cudaMalloc(&L->reinit_dev, sizeof(int)));
+  CKF(dmalloc(L, &L->reinit_dev, sizeof(int)));
   CKF(cudaMemsetAsync(L->reinit_dev, 0, sizeof(int), L->st));
-  CKF(cudaMalloc(&L->step_dev, sizeof(int64_t)));
+  CKF(dmalloc(L, &L->step_dev, sizeof(int64_t)));
   CKF(cudaMemsetAsync(L->step_dev, 0, sizeof(int64_t), L->st));
   CKF(cudaMallocHost(&L->loss_host, 2 * sizeof(double)));
-  CKF(cudaMalloc(&L->flags_dev, 2 * sizeof(int)));
+  CKF(dmalloc(L, &L->flags_dev, 2 * sizeof(int)));
   CKF(cudaMemsetAsync(L->flags_dev, 0, 2 * sizeof(int), L->st));
   CKF(cudaMallocHost(&L->flags_host, 2 * sizeof(int)));
   L->flags_host[0] = L->flags_host[1] = 0;
   if (cfg->keep_grads) {
-    CKF(cudaMalloc(&L->gW, F * k * wp * 4));
+    CKF(dmalloc(L, &L->gW, F * k * wp * 4));
     CKF(cudaMemsetAsync(L->gW, 0, F * k * wp * 4, L->st));
-    CKF(cudaMalloc(&L->galpha, F * 4));
-    CKF(cudaMalloc(&L->gb, F * n * 4));
+    CKF(dmalloc(L, &L->galpha, F * 4));
+    CKF(dmalloc(L, &L->gb, F * n * 4));
   }
   if (cfg->precision == LCAE_FP32) {
-    CKF(cudaMalloc(&L->xt32, m * img * 4));
+    CKF(dmalloc(L, &L->xt32, m * img * 4));
     FAIL(f32_alloc(L));
   } else {
-    CKF(cudaMalloc(&L->xt16, mp * img * 2));
+    CKF(dmalloc(L, &L->xt16, mp * img * 2));
     CKF(cudaMemset(L->xt16, 0, mp * img * 2));   // padded batch columns stay zero
-    CKF(cudaMalloc(&L->rowsq, F * k * 4));
+    CKF(dmalloc(L, &L->rowsq, F * k * 4));
     FAIL(tc_alloc(L));
   }
   // model parallel: world_size > 1; or one rank with an NCCL id (the whole layer as a single tile: exercises the
@@ -408,7 +410,7 @@ lcae_status lcae_prefetch_input(lcae_layer *L, const float *x_host) {
   if (is_device_ptr(x_host)) return LCAE_OK;   // nothing to copy
   const size_t bytes = input_elems(L) * 4;
   if (!L->x_pf) {   // first use: the buffer, a copy stream and two events
-    LCAE_CK(cudaMalloc(&L->x_pf, bytes));
+    LCAE_CK(dmalloc(L, &L->x_pf, bytes));
     LCAE_CK(cudaStreamCreateWithFlags(&L->copy_st, cudaStreamNonBlocking));
     LCAE_CK(cudaEventCreateWithFlags(&L->pf_done, cudaEventDisableTiming));
     LCAE_CK(cudaEventCreateWithFlags(&L->x_consumed, cudaEventDisableTiming));
@@ -563,3 +565,19 @@ lcae_status lcae_profile_read(lcae_layer *L, double *main_kernel_ms, int32_t *la
 }
 
 }  // extern "C"
+
+// ---- dev hook (sanitizer substitute): count allocations whose 4 KB canary tail was overwritten (LCAE_DEV_CANARY)
+extern "C" lcae_status lcae_dev_check_canaries(lcae_layer *L, int64_t *bad_allocs, int64_t *checked) {
+  if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
+  LCAE_CK(cudaDeviceSynchronize());
+  std::vector<unsigned char> tail(CANARY_BYTES);
+  int64_t bad = 0;
+  for (auto &a : L->allocs) {
+    LCAE_CK(cudaMemcpy(tail.data(), reinterpret_cast<char *>(a.first) + a.second, CANARY_BYTES, cudaMemcpyDeviceToHost));
+    for (unsigned char c : tail)
+      if (c != 0xA5) { ++bad; break; }
+  }
+  if (bad_allocs) *bad_allocs = bad;
+  if (checked) *checked = (int64_t)L->allocs.size();
+  return LCAE_OK;
+}

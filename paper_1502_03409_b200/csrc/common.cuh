@@ -4,6 +4,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/lcae.h"
 
@@ -102,12 +104,46 @@ struct lcae_layer {
   lcae::F32Scratch f32;
   lcae::TcScratch *tc = nullptr;
   lcae::MpState *mpst = nullptr;   // model-parallel state (world_size > 1)
+  // dev checks (sanitizer substitute, include/lcae.h is unaffected): LCAE_DEV_POISON=1 fills every allocation
+  // with 0xFF bytes (NaN) so that a read before write shows up in the results; LCAE_DEV_CANARY=1 pads every
+  // allocation with a 4 KB 0xA5 tail that lcae_dev_check_canaries verifies (out-of-bounds writes)
+  int poison = 0, canary = 0;
+  std::vector<std::pair<void *, size_t>> allocs;
   // profiling (lcae_profile): events around the dominant kernel
   int prof_on = 0, prof_n = 0;
   cudaEvent_t *prof_ev = nullptr;   // [2 * 4096]
 };
 
 namespace lcae {
+
+constexpr size_t CANARY_BYTES = 4096;
+
+// Device-side bounds checks of the checked build (LCAE_CHECKED; no code in the production build).
+#ifdef LCAE_CHECKED
+#define LCAE_DCHECK(cond)                                                                                  \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("lcae check failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, blockIdx.x, threadIdx.x, \
+             #cond);                                                                                       \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define LCAE_DCHECK(cond) do { } while (0)
+#endif
+
+// Every device allocation of a layer goes through here (dev poison / canary modes above).
+template <typename T>
+inline cudaError_t dmalloc(lcae_layer *L, T **p, size_t bytes) {
+  cudaError_t e = cudaMalloc(reinterpret_cast<void **>(p), bytes + (L->canary ? CANARY_BYTES : 0));
+  if (e != cudaSuccess) return e;
+  if (L->poison && (e = cudaMemset(*p, 0xFF, bytes)) != cudaSuccess) return e;
+  if (L->canary) {
+    if ((e = cudaMemset(reinterpret_cast<char *>(*p) + bytes, 0xA5, CANARY_BYTES)) != cudaSuccess) return e;
+    L->allocs.emplace_back(*p, bytes);
+  }
+  return cudaSuccess;
+}
 
 __host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 

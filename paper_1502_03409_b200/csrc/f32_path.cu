@@ -284,15 +284,15 @@ lcae_status f32_alloc(lcae_layer *L) {
   F32Scratch &s = L->f32;
   s.Fc = Fc;
   size_t km = (size_t)Fc * g.k * g.m, nm = (size_t)Fc * g.n * g.m;
-  LCAE_CK(cudaMalloc(&s.U, km * 4));
-  LCAE_CK(cudaMalloc(&s.H, km * 4));
-  LCAE_CK(cudaMalloc(&s.Q, km * 4));
-  LCAE_CK(cudaMalloc(&s.G, km * 4));
-  LCAE_CK(cudaMalloc(&s.R, nm * 4));
-  LCAE_CK(cudaMalloc(&s.dXp, nm * 4));
-  LCAE_CK(cudaMalloc(&s.dW, (size_t)Fc * g.k * g.n * 4));
-  LCAE_CK(cudaMalloc(&s.da, (size_t)Fc * 4));
-  LCAE_CK(cudaMalloc(&s.db, (size_t)Fc * g.n * 4));
+  LCAE_CK(dmalloc(L, &s.U, km * 4));
+  LCAE_CK(dmalloc(L, &s.H, km * 4));
+  LCAE_CK(dmalloc(L, &s.Q, km * 4));
+  LCAE_CK(dmalloc(L, &s.G, km * 4));
+  LCAE_CK(dmalloc(L, &s.R, nm * 4));
+  LCAE_CK(dmalloc(L, &s.dXp, nm * 4));
+  LCAE_CK(dmalloc(L, &s.dW, (size_t)Fc * g.k * g.n * 4));
+  LCAE_CK(dmalloc(L, &s.da, (size_t)Fc * 4));
+  LCAE_CK(dmalloc(L, &s.db, (size_t)Fc * g.n * 4));
   return LCAE_OK;
 }
 

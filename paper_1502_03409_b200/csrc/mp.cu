@@ -276,12 +276,12 @@ lcae_status mp_init(lcae_layer *L, const Geo &gg) {
   }
   const size_t es = elem_size(L);
   if (M->in_send_n) {
-    LCAE_CK(cudaMalloc(&M->in_send_buf, M->in_send_n * es));
-    LCAE_CK(cudaMalloc(&M->dx_recv_buf, M->in_send_n * 4));
+    LCAE_CK(dmalloc(L, &M->in_send_buf, M->in_send_n * es));
+    LCAE_CK(dmalloc(L, &M->dx_recv_buf, M->in_send_n * 4));
   }
   if (M->in_recv_n) {
-    LCAE_CK(cudaMalloc(&M->in_recv_buf, M->in_recv_n * es));
-    LCAE_CK(cudaMalloc(&M->dx_send_buf, M->in_recv_n * 4));
+    LCAE_CK(dmalloc(L, &M->in_recv_buf, M->in_recv_n * es));
+    LCAE_CK(dmalloc(L, &M->dx_send_buf, M->in_recv_n * 4));
   }
   // interior fields (window inside the owned pixels: computable before the halo arrives), then boundary fields
   const int oh = M->t.own[1] - M->t.own[0], ow = M->t.own[3] - M->t.own[2];
@@ -294,7 +294,7 @@ lcae_status mp_init(lcae_layer *L, const Geo &gg) {
       if (pass == 0 && inside) ++M->n_int;
     }
   M->n_bnd = g.F - M->n_int;
-  LCAE_CK(cudaMalloc(&M->flist, fl.size() * sizeof(int)));
+  LCAE_CK(dmalloc(L, &M->flist, fl.size() * sizeof(int)));
   LCAE_CK(cudaMemcpy(M->flist, fl.data(), fl.size() * sizeof(int), cudaMemcpyHostToDevice));
   LCAE_CK(cudaStreamCreateWithFlags(&M->cs, cudaStreamNonBlocking));
   LCAE_CK(cudaEventCreateWithFlags(&M->ev_staged, cudaEventDisableTiming));

@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace lcae {
 namespace ptx {
@@ -40,6 +41,28 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+#ifdef LCAE_CHECKED
+// Checked build (liblcae_checked.so; the sanitizer substitute): every mbarrier wait has a
+// watchdog -- a phase that has not completed after ~2^34 cycles (~9 s) reports the barrier and traps instead of
+// hanging the GPU.
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+               : "=r"(ok)
+               : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+               : "memory");
+  return ok != 0;
+}
+static __device__ __noinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  const long long t0 = clock64();
+  while (!mbar_try(bar, parity))
+    if (clock64() - t0 > (1ll << 34)) {
+      printf("lcae watchdog: block %d thread %d waits on mbarrier smem+0x%x parity %u\n", blockIdx.x, threadIdx.x,
+             smem_u32(bar), parity);
+      __trap();
+    }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n"
@@ -49,6 +72,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "r"(parity), "r"(0x989680u)
       : "memory");
 }
+#endif
 // Spin-free wait for waiters that are themselves latency-critical consumers: same instruction, no hint.
 __device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
   asm volatile(

@@ -155,17 +155,17 @@ lcae_status tc_alloc(lcae_layer *L) {
   // (the cross-field barrier phases and buffer reuse of the production kernel, checked against the oracle)
   if (const char *e = getenv("LCAE_DEV_MAX_CLUSTERS")) ncl = std::max(1, std::min(ncl, atoi(e)));
   s->grid = ncl * s->CB;
-  LCAE_CK(cudaMalloc(&s->loss_part, (size_t)g.F * s->CB * 2 * sizeof(double)));
-  LCAE_CK(cudaMalloc(&s->da_part, (size_t)g.F * s->CB * 4));
-  LCAE_CK(cudaMalloc(&s->db_part, (size_t)g.F * s->CB * g.n * 4));
-  LCAE_CK(cudaMalloc(&s->rowsq_part, (size_t)g.F * s->CB * 2 * tc::KP * 4));
-  LCAE_CK(cudaMalloc(&s->dbscr, (size_t)s->grid * 4 * tc::MAX_NPAD * 4));   // per-CTA db partials (L2)
-  LCAE_CK(cudaMalloc(&s->dscr, (size_t)s->grid * T * 16384));   // per-CTA pass-1 delta tiles (L2-resident)
-  LCAE_CK(cudaMalloc(&s->trace, 48 * sizeof(unsigned long long)));
+  LCAE_CK(dmalloc(L, &s->loss_part, (size_t)g.F * s->CB * 2 * sizeof(double)));
+  LCAE_CK(dmalloc(L, &s->da_part, (size_t)g.F * s->CB * 4));
+  LCAE_CK(dmalloc(L, &s->db_part, (size_t)g.F * s->CB * g.n * 4));
+  LCAE_CK(dmalloc(L, &s->rowsq_part, (size_t)g.F * s->CB * 2 * tc::KP * 4));
+  LCAE_CK(dmalloc(L, &s->dbscr, (size_t)s->grid * 4 * tc::MAX_NPAD * 4));   // per-CTA db partials (L2)
+  LCAE_CK(dmalloc(L, &s->dscr, (size_t)s->grid * T * 16384));   // per-CTA pass-1 delta tiles (L2-resident)
+  LCAE_CK(dmalloc(L, &s->trace, 48 * sizeof(unsigned long long)));
   LCAE_CK(cudaMemset(s->trace, 0, 48 * sizeof(unsigned long long)));
   // Wb is [F][KP][n_al] (pad rows zero) for the bf16 path
   cudaFree(L->Wb);
-  LCAE_CK(cudaMalloc(&L->Wb, (size_t)g.F * tc::KP * L->n_al * 2));
+  LCAE_CK(dmalloc(L, &L->Wb, (size_t)g.F * tc::KP * L->n_al * 2));
   LCAE_CK(cudaMemset(L->Wb, 0, (size_t)g.F * tc::KP * L->n_al * 2));
   if (!make_tmap_2d_bf16(&s->tmW, L->Wb, (uint64_t)g.F * tc::KP, (uint64_t)L->n_al, (uint64_t)L->n_al, tc::KP)) {
     set_error("cuTensorMapEncodeTiled failed for W");
@@ -195,14 +195,14 @@ lcae_status tc_alloc(lcae_layer *L) {
         return LCAE_ERR_CONFIG;
       }
     }
-  LCAE_CK(cudaMalloc(&s->dxpieces, dpc.size() * 4));
+  LCAE_CK(dmalloc(L, &s->dxpieces, dpc.size() * 4));
   LCAE_CK(cudaMemcpy(s->dxpieces, dpc.data(), dpc.size() * 4, cudaMemcpyHostToDevice));
   for (int i = 0; i < tc::NDMAP; ++i)
     if (!make_tmap_2d_f32(&s->tmD[i], L->dxt, prow, (uint64_t)L->mp, (uint64_t)L->mp, 1u << i, 32)) {
       set_error("cuTensorMapEncodeTiled failed for dX");
       return LCAE_ERR_CUDA;
     }
-  LCAE_CK(cudaMalloc(&s->xpieces, pcs.size() * 4));
+  LCAE_CK(dmalloc(L, &s->xpieces, pcs.size() * 4));
   LCAE_CK(cudaMemcpy(s->xpieces, pcs.data(), pcs.size() * 4, cudaMemcpyHostToDevice));
   return LCAE_OK;
 }

@@ -106,7 +106,8 @@ struct __align__(1024) Smem {
   uint64_t uf[4], ue[4];     // encode-only mode: 4 U buffers in TMEM (full / free)
   uint64_t r_full[NRB], r_empty[NRB], dl_full[2], dl_empty[2];
   uint64_t p2_full[NB2], p2_empty[NB2], d2full[2], d2empty[2];
-  uint64_t recv_full, peer_free;
+  uint64_t recv_full[NEPI], peer_free[NEPI];   // per epilogue warp: the dW exchange couples warp w of the two
+                                               // CTAs only (not all 16 warps of the pair)
   uint32_t tmem_base;
   unsigned long long tr[48];   // optional wait-cycle / section trace (lcae_dev_trace)
 };
@@ -194,7 +195,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
   // parameters: every CTA reads the same flags (written by earlier kernels), so all return together
   if (step && (P.flags[0] | P.flags[1])) return;
   const int nfl = P.flist ? P.nfl : P.g.F;
-  auto fid = [&](int i) { return P.flist ? __ldg(P.flist + i) : i; };
+  auto fid = [&](int i) {
+    const int f_ = P.flist ? __ldg(P.flist + i) : i;
+    LCAE_DCHECK(f_ >= 0 && f_ < P.g.F);
+    return f_;
+  };
+  const int64_t prow = (int64_t)P.g.H * P.g.W * P.g.C;   // pixel-feature rows of the HWCN image (checked build)
+  (void)prow;
   // trace: lane 0 of the producers / MMA warp and of epilogue warp 2 record their barrier-wait cycles
   const bool trec = TR && P.trace != nullptr && lane == 0 && (warp <= 2 || warp == XWARP);
   const long long t_start = clock64();
@@ -250,8 +257,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       ptx::mbar_init(&S.d2full[i], 1);
       ptx::mbar_init(&S.d2empty[i], 1);
     }
-    ptx::mbar_init(&S.recv_full, 1);   // armed per tile with expect_tx; completed by the peer's st.async bytes
-    ptx::mbar_init(&S.peer_free, NEPI);
+    for (int i = 0; i < NEPI; ++i) {
+      ptx::mbar_init(&S.recv_full[i], 1);   // armed per tile with expect_tx; completed by the peer's st.async bytes
+      ptx::mbar_init(&S.peer_free[i], 1);   // the peer's warp i has read its receive slice
+    }
     ptx::fence_mbar_init();
   }
   ptx::fence_proxy_async_smem();   // -I tile is read by the tensor core
@@ -328,6 +337,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           const uint32_t w = e ? w1 : w0;
           if (w != 0xFFFFFFFFu) {
             const int offp = (int)(w & 0xFFFFu), dr = (int)((w >> 16) & 0xFFu), lg = (int)(w >> 24);
+            LCAE_DCHECK(lg < NXMAP && dr + (1 << lg) <= NT && pixbase + offp + (1 << lg) <= prow);
 #pragma unroll
             for (int h = 0; h < 2; ++h)
               ptx::tma_load_2d(dst_tile + h * 8192 + dr * 128, &P.tmX[lg], bar, s0 + 64 * h, pixbase + offp);
@@ -550,8 +560,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     uint32_t nf = 0, ur = 0, ud = 0, u2 = 0;
     // cluster-peer addresses of the dW exchange, mapped once (mapa is an MIO round trip)
     const uint32_t peer_recv = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.recv[half][row][0]), crank ^ 1u) : 0u;
-    const uint32_t peer_recv_full = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.recv_full), crank ^ 1u) : 0u;
-    const uint32_t peer_free_bar = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.peer_free), crank ^ 1u) : 0u;
+    const uint32_t peer_recv_full = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.recv_full[ew]), crank ^ 1u) : 0u;
+    const uint32_t peer_free_bar = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.peer_free[ew]), crank ^ 1u) : 0u;
     for (int fi = cid; fi < nfl; fi += ncl, ++nf) {
       const int f = fid(fi);
       const int fr = f / g.gc, fc = f - fr * g.gc;
@@ -675,7 +685,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&S.dl_full[db_]);
           ++ud;
-          // db partial: column sums over this warp's 32 samples (butterfly transpose-reduce: lane l <- column l)
+          // db partial: column sums over this warp's 32 samples (butterfly transpose-reduce: lane l <- column l;
+          // measured faster than a transpose through the staging slice, whose loads wait behind the stores)
 #pragma unroll
           for (int o = 16, w = 16; o >= 1; o >>= 1, w >>= 1) {
             const bool up = lane & o;
@@ -686,8 +697,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               rv[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
             }
           }
+          const float dsum = rv[0];
           // this lane quarter's partial; the four quarters are summed once per field (no per-tile barrier)
-          P.dbscr[((size_t)blockIdx.x * 4 + qd) * MAX_NPAD + j * NT + hc + lane] = rv[0];
+          LCAE_DCHECK(j * NT + hc + lane < MAX_NPAD);
+          P.dbscr[((size_t)blockIdx.x * 4 + qd) * MAX_NPAD + j * NT + hc + lane] = dsum;
         }
       }
       if (step) {
@@ -775,6 +788,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             for (int c = 0; c < 16; ++c) stg[c * 32 + lane] = xv[16 * r + c];
             ptx::fence_proxy_async_smem();
             __syncwarp();
+            LCAE_DCHECK(pw == 0xFFFFFFFFu || ((pw >> 24) < (uint32_t)NDMAP && ((pw >> 16) & 0xFFu) + (1u << (pw >> 24)) <= 16u &&
+                                             pixbase + (pw & 0xFFFFu) + (1u << (pw >> 24)) <= prow));
             if (pw != 0xFFFFFFFFu && do_red)
               ptx::tma_red_add_2d(&P.tmD[pw >> 24], stg + ((pw >> 16) & 0xFFu) * 32, s0 + qd * 32,
                                   (int)pixbase + (int)(pw & 0xFFFFu));
@@ -816,9 +831,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               ptx::tmem_ld16(tl + base + 64 + hc + 16 * crank, dw);
               ptx::tmem_ld16(tl + base + 64 + hc + 16 * (1 - crank), dw + 16);
               ptx::tmem_ld_wait();
-              // arm this tile's receive phase: 8 warps x 32 rows x 16 floats arrive from the peer via st.async
-              if (etid == 0) ptx::mbar_arrive_expect_tx(&S.recv_full, 2 * 128 * 16 * 4);
-              TWAIT(22, ptx::mbar_wait(&S.peer_free, (u2 & 1) ^ 1));
+              // arm this warp's receive phase: 32 rows x 16 floats arrive from the peer's warp ew via st.async
+              if (lane == 0) ptx::mbar_arrive_expect_tx(&S.recv_full[ew], 32 * 16 * 4);
+              TWAIT(22, ptx::mbar_wait(&S.peer_free[ew], (u2 & 1) ^ 1));
 #pragma unroll
               for (int t = 0; t < 4; ++t)
                 ptx::st_async_v4(peer_recv + 16 * (t ^ swr),
@@ -845,7 +860,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             TMARK(36);
             TMARK(41);
             // + the peer's batch slice, read straight from the receive slice in the same layout
-            TWAIT(22, ptx::mbar_wait(&S.recv_full, u2 & 1));
+            TWAIT(22, ptx::mbar_wait(&S.recv_full[ew], u2 & 1));
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const int r = 8 * i + rr, o = r * 16 + 4 * (cq ^ ((r >> 1) & 3));
@@ -897,6 +912,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
                 if (!rok[i] || cc0 >= P.wp) continue;
                 const int r = qd * 32 + 8 * i + rr;
                 float *wp_ = const_cast<float *>(wrp[i]) + j * NT + 16 * h;   // = W~ + row * wp + cc0
+                LCAE_DCHECK(wp_ >= P.W && wp_ + 4 <= P.W + (int64_t)g.F * k * P.wp && cc0 + 4 <= P.wp);
+                LCAE_DCHECK(((int64_t)f * KP + r) * P.n_al + cc0 + 4 <= (int64_t)g.F * KP * P.n_al || cc0 >= P.n_al);
                 const float d0[4] = {dq[4 * h + i].x, dq[4 * h + i].y, dq[4 * h + i].z, dq[4 * h + i].w};
                 const float wo4[4] = {wv[4 * h + i].x, wv[4 * h + i].y, wv[4 * h + i].z, wv[4 * h + i].w};
                 float d[4], wn[4], vo[4] = {0.f, 0.f, 0.f, 0.f};
@@ -943,6 +960,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         for (int t = etid; t < n; t += 32 * NEPI)
           P.db_part[((int64_t)f * CB + crank) * n + t] = ((d[t] + d[MAX_NPAD + t]) + d[2 * MAX_NPAD + t]) + d[3 * MAX_NPAD + t];
       }
+      LCAE_DCHECK(f < g.F && (int)crank < CB);
       if (etid == 0) {
         double a0 = 0.0, a1 = 0.0;
         float a2 = 0.f;

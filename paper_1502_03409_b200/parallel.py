@@ -16,9 +16,13 @@ exists) and a rectangle of image pixels.  One step on a rank:
      (lcae_region_add on the GPU);
   4. (optional) loss all-reduce (sum).
 
-The exchange logic is plain host code over torch.distributed point-to-point ops, so it runs over NCCL on GPUs
-(one process per GPU) and over gloo on CPU; tests/test_parallel_cpu.py drives it with world_size 2 on CPU.
-Byte counts of every exchange are recorded and checked against the static prediction.
+On GPUs this whole step runs INSIDE the library (include/lcae.h world_size > 1, csrc/mp.cu: NCCL send / recv of
+bf16 halos overlapping the interior fields, fp32 dX returns, loss all-reduce); bench.py uses that path and
+tests/test_abi_cpu.py checks that the library's tiling (lcae_geometry own_px / own_fields) equals plan() below.
+This module is the host-side statement of the same plan, and HaloExchange is the same exchange written over
+torch.distributed point-to-point ops: tests/test_parallel_cpu.py drives it over gloo (world_size 2 and 4, CPU)
+with the oracle as the per-rank engine. Byte counts of every exchange are recorded and checked against the
+static prediction, which the library's exchange buffers also match (tests/test_gpu_mp.py).
 """
 from __future__ import annotations
 
@@ -196,49 +200,3 @@ def tile_shape(shape, tile: Tile):
     """The LayerShape of the rank-local layer: its image is the tile's `need` region."""
     h, w = tile.need_hw
     return shape.replace(name=f"{shape.name}-r{tile.rank}", img_h=h, img_w=w)
-
-
-class TileRunner:
-    """GPU runner of one rank's tile through the C ABI (bench.py and multi-GPU tests)."""
-
-    def __init__(self, shape, tile: Tile, world: int, rank: int, seed: int = 0, precision=None, stream=None):
-        import torch
-        from . import lcae
-        from .inputs import make_images, make_params
-        self.shape, self.tile, self.rank = shape, tile, rank
-        self.tiles = plan(shape, world)
-        self.hx = HaloExchange(self.tiles, rank)
-        ts = tile_shape(shape, tile)
-        self.local_shape = ts
-        cfg = lcae.make_config(ts, precision=lcae.BF16 if precision is None else precision,
-                               stream=stream, field_row0=tile.fields_r[0], field_col0=tile.fields_c[0],
-                               global_grid_c=shape.grid_c)
-        self.layer = lcae.Layer(cfg)
-        gr, gc = tile.grid
-        fids = [(tile.fields_r[0] + r) * shape.grid_c + tile.fields_c[0] + c for r in range(gr) for c in range(gc)]
-        W, a, b = make_params(shape, seed=seed, fields=fids)
-        self.layer.set_params(W, a, b)
-        del W
-        full = make_images(shape, seed=1)
-        o = tile.own
-        self.x_own = torch.from_numpy(full[:, o[0]:o[1], o[2]:o[3], :].copy()).cuda()
-        h, w = tile.need_hw
-        self.x_ext = torch.empty((shape.batch, h, w, shape.img_c), dtype=torch.float32, device="cuda")
-        self.dx_ext = torch.empty_like(self.x_ext)
-        self.dx_own = torch.empty_like(self.x_own)
-        self.extra_launches = 0
-        self._lcae = lcae
-
-    def _add(self, dst, src, y0, x0):
-        import torch
-        self._lcae.region_add(dst, src, y0, x0, stream=torch.cuda.current_stream().cuda_stream)
-        self.extra_launches += 1
-
-    def step(self):
-        self.extra_launches = 0
-        self.hx.gather_input(self.x_own, self.x_ext)
-        self.layer.step(self.x_ext, self.dx_ext, want_loss=False)
-        self.hx.return_dx(self.dx_ext, self.dx_own, self._add)
-
-    def bench_step_fn(self, stream):
-        return lambda i: self.step()

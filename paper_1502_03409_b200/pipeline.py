@@ -8,7 +8,13 @@ and replays the data from block 0 (Fig. 3). A deterministic sequential scheduler
 block per active trainer per tick, bottom layer first), so a run is reproducible bit for bit.
 
 The scheduler is host logic over an engine with the layer operations; `LcaeEngine` runs them on the GPU
-through the C ABI (lcae_step / lcae_encode / lcae_lcn / parameter copies between layer instances).
+through the C ABI (lcae_step / lcae_encode / lcae_lcn / parameter copies between layer instances), one call
+after the other on one stream. `StreamEngine` runs them SIMULTANEOUSLY ("two instances of the
+layer L are run simultaneously"): every layer instance (trainer or forwarder) owns a CUDA stream, a tick
+enqueues every active layer's work without waiting (forwarder chains on the forwarders' streams, trainer steps
+on the trainers' streams, ordered only by their data dependencies through CUDA events), and the host reads the
+losses once per tick -- except when a start decision needs the current objective. The decisions, and therefore
+every parameter bit, are those of the sequential schedule (tests/test_gpu_pipeline.py).
 """
 from dataclasses import dataclass, field
 from typing import List, Optional
@@ -84,9 +90,26 @@ def run_pipeline(engine, shapes, blocks, cfg: PipelineConfig, seed=0):
         b.source_block = done[l]
 
     def input_of(l, x):
+        if getattr(engine, "concurrent", False):
+            return engine.chain(l, [fwd[i].handle for i in range(l)], x, trainers[l])
         for i in range(l):
             x = engine.lcn(engine.encode(fwd[i].handle, x))
         return x
+
+    concurrent = getattr(engine, "concurrent", False)
+    if concurrent:
+        engine.begin()   # inputs created on other streams are complete before the layer streams read them
+    pending = []   # (layer, record, lazy loss) of this tick, resolved in order
+
+    def resolve(upto_layer=None):
+        keep = []
+        for l_, rec, h in pending:
+            if upto_layer is None or l_ == upto_layer:
+                rec.objective = engine.loss(h)
+                hist[l_].append(rec.objective)
+            else:
+                keep.append((l_, rec, h))
+        pending[:] = keep
 
     while any(active[l] and done[l] < total for l in range(n)):
         for l in range(n):                              # one block per active trainer, bottom layer first
@@ -95,13 +118,19 @@ def run_pipeline(engine, shapes, blocks, cfg: PipelineConfig, seed=0):
             x = input_of(l, blocks[done[l] % len(blocks)])
             versions = tuple(fwd[i].version for i in range(l))
             stale = max([done[i] - fwd[i].source_block for i in range(l)], default=0)
-            J = engine.step(trainers[l], x)
-            log.records.append(LogRecord(l, done[l], J, versions, stale))
-            hist[l].append(J)
+            rec = LogRecord(l, done[l], None, versions, stale)
+            log.records.append(rec)
+            if concurrent:   # enqueue only; the objective is read at the end of the tick (or when needed)
+                pending.append((l, rec, engine.step_async(trainers[l], x)))
+            else:
+                rec.objective = engine.step(trainers[l], x)
+                hist[l].append(rec.objective)
             done[l] += 1
             if l + 1 < n:
                 started = active[l + 1]
                 finished = done[l] >= total
+                if not started and done[l] >= cfg.warmup_blocks:
+                    resolve(l)   # the start test needs this block's objective
                 ready = done[l] >= cfg.warmup_blocks and stabilized(hist[l], cfg.stabilization_window,
                                                                    cfg.stabilization_rel_tol)
                 if not started and (ready or finished):
@@ -109,6 +138,7 @@ def run_pipeline(engine, shapes, blocks, cfg: PipelineConfig, seed=0):
                     active[l + 1] = True
                 elif started and (done[l] - fwd[l].source_block >= cfg.sync_period_blocks or finished):
                     sync(l)
+        resolve()
     return trainers, log
 
 
@@ -162,3 +192,75 @@ class LcaeEngine:
         for L in self.layers:
             L.close()
         self.layers = []
+
+
+class StreamEngine(LcaeEngine):
+    """Concurrent execution of the Fig. 3 pipeline: one CUDA stream per layer instance, dependencies through
+    events only ("run simultaneously"). Trainer l's step, forwarder l's encode for layer l+1 and
+    the other layers' work of the same tick overlap on the GPU."""
+    concurrent = True
+
+    def __init__(self, precision=None, lcn_window=3, lcn_floor=1e-4):
+        super().__init__(precision, lcn_window, lcn_floor)
+        self.bufs = {}
+
+    def make_layer(self, shape, seed):
+        import torch
+        from .inputs import make_params
+        st = torch.cuda.Stream()
+        L = self.lcae.Layer(self.lcae.make_config(shape, precision=self.precision, stream=st.cuda_stream))
+        W, a, b = make_params(shape, seed=seed)
+        L.set_params(W, a, b)
+        L.shape, L.stream, L.done = shape, st, None
+        self.layers.append(L)
+        return L
+
+    def _buf(self, key, shape):
+        import torch
+        if key not in self.bufs:
+            self.bufs[key] = torch.empty(shape, dtype=torch.float32, device="cuda")
+        return self.bufs[key]
+
+    def begin(self):
+        import torch
+        torch.cuda.synchronize()
+
+    def chain(self, l, fwds, x, consumer):
+        """Layer l's input: x through forwarders 0..l-1 (encode + LCN on each forwarder's stream), into buffers
+        owned by layer l; returns (tensor, event). The chain starts after layer l's previous step (its buffers
+        are free again)."""
+        import torch
+        ev = None
+        for i, F in enumerate(fwds):
+            s = F.shape
+            st = F.stream
+            if i == 0 and consumer.done is not None:
+                st.wait_event(consumer.done)
+            if ev is not None:
+                st.wait_event(ev)
+            code = self._buf((l, i, "p"), (s.batch, s.grid_r, s.grid_c, s.filters // s.pool_group))
+            y = self._buf((l, i, "y"), code.shape)
+            scratch = self._buf((l, i, "s"), (2 * code.numel(),))
+            with torch.cuda.stream(st):
+                F.encode(x, code, want_loss=False)
+                self.lcae.lcn(code, y, scratch, self.window, self.floor, st.cuda_stream)
+            ev = st.record_event()
+            x = y
+        return (x, ev)
+
+    def step_async(self, L, xe):
+        x, ev = xe if isinstance(xe, tuple) else (xe, None)
+        if ev is not None:
+            L.stream.wait_event(ev)
+        L.step(x, None, want_loss=False)
+        L.done = L.stream.record_event()
+        return L
+
+    def loss(self, L):
+        jr, js = L.last_loss()   # synchronises this layer's stream only
+        return jr + js
+
+    def copy_params(self, src, dst):
+        # the snapshot is taken after the trainer's enqueued steps (get_params runs on, and waits for, the
+        # trainer's stream) and lands before the forwarder's next encode (set_params waits for its stream)
+        super().copy_params(src, dst)

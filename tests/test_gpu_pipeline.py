@@ -67,3 +67,35 @@ def test_pipelined_run_staleness_gpu():
         assert recs and [r.block for r in recs] == list(range(len(recs)))
         assert all(r.staleness <= pc.sync_period_blocks for r in recs)
         assert all(np.isfinite(r.objective) for r in recs)
+
+
+def test_concurrent_streams_equal_sequential_schedule():
+    """StreamEngine (one CUDA stream per layer instance, trainer and forwarder running simultaneously,
+    PAPER.md:111) makes the same decisions and the same parameter bits as the one-stream schedule."""
+    import time
+
+    import torch
+    from paper_1502_03409_b200.pipeline import LcaeEngine, PipelineConfig, StreamEngine, run_pipeline
+    shapes = desk_stack(batch=16).shapes
+    blocks = [torch.from_numpy(make_images(shapes[0], seed=400 + i)).cuda() for i in range(5)]
+    pc = PipelineConfig(warmup_blocks=4, sync_period_blocks=3, stabilization_window=2, stabilization_rel_tol=10.0,
+                        epochs_per_layer=6)
+    out = {}
+    for name, cls in (("sequential", LcaeEngine), ("streams", StreamEngine)):
+        eng = cls()
+        try:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            trainers, log = run_pipeline(eng, shapes, blocks, pc)
+            torch.cuda.synchronize()
+            out[name] = ([_params(L) for L in trainers], log, time.perf_counter() - t0)
+        finally:
+            eng.close()
+    (pa, la, ta), (pb, lb, tb) = out["sequential"], out["streams"]
+    for x, y in zip(pa, pb):
+        for u, v in zip(x, y):
+            assert np.array_equal(u, v)
+    assert la.lines() == lb.lines()
+    assert any(r.layer == 2 for r in lb.records)
+    print(f"pipeline wall time: one stream {ta * 1e3:.1f} ms, concurrent streams {tb * 1e3:.1f} ms "
+          f"({len(lb.records)} layer-blocks)")

@@ -90,6 +90,19 @@ def test_bf16_trained_regime(name, raw):
     X = make_images(shape, seed=12, bf16_round=not raw)
     out = gpu_step(shape, 1, W1, a1, b1, X)
     o = oracle_step(shape, W1, a1, b1, X)
+    # dalpha_f = sum_ij D_ij U_ij cancels towards 0 as alpha approaches its optimum, so its relative error grows
+    # without bound while the rounding error stays ~ u * sum |D (.) U| (the bf16 delta and D operands): dalpha
+    # and the alpha update are held to the tolerance relative to that sum of magnitudes (R22);
+    # every other tensor keeps the normwise bound (R10).
+    scale = np.array([O.rica_field(W1[f], float(a1[f]), b1[f], _patches(shape, X, f), shape.lam, shape.eps,
+                                   shape.pool_group)["dalpha_abs"] for f in range(shape.fields)])
+    da_err = np.abs(out["dalpha"] - o["dalpha"]) / scale
+    au_err = np.abs((out["alpha_new"].astype(np.float64) - a1) - (o["alpha_new"] - a1)) / (shape.lr * scale)
+    print(name, "dalpha normwise", f"{normwise(out['dalpha'], o['dalpha']):.1e}", "vs sum|D U|",
+          f"{da_err.max():.1e}", "alpha update", f"{au_err.max():.1e}")
+    assert da_err.max() <= 2e-2 and au_err.max() <= 2e-2
+    out = {k_: v for k_, v in out.items() if k_ != "dalpha"}
+    out["alpha_new"] = o["alpha_new"].astype(np.float32)   # checked above against its own error scale
     errs = _compare(shape, 1, out, o, W1.astype(np.float64), a1.astype(np.float64), b1.astype(np.float64))
     print(name, {k_: f"{v:.1e}" for k_, v in errs.items()})
 
