@@ -293,7 +293,32 @@ def run_infer(args, shape):
 # SURVEY.md §8(d) c5 "15 B point": the paper's parameter count ("15 billion parameters") as one
 # c3-shaped layer, 347 x 348 fields of 18 x 18 x 3 -> 128 filters (15.02 B weights), batch 256, on ONE GPU
 # (fp32 master + bf16 shadow ~ 6 B/param = 90 GB of the 180 GB HBM). Weights are initialised on the device.
-EXTRA = {"c15b": LayerShape("c15b", 710, 712, 3, 18, 18, 2, 128, 1, 256, lr=1e-3 / 256)}
+EXTRA = {"c15b": LayerShape("c15b", 710, 712, 3, 18, 18, 2, 128, 1, 256, lr=1e-3 / 256),
+         # SURVEY.md §8(d) c3': the paper-exact layer 1 (16 x 16 x 3 receptive fields, stride 4 ->
+         # 4 x 4 x 24 = 384 filters per field; PAPER.md:111 mini-batch 192) on 300 x 300 x 3 images: 72 x 72 =
+         # 5184 fields, 1.53 B weights. k = 384 exceeds the fused bf16 kernel's TMEM budget (k <= 128), so it runs
+         # on the fp32 path (--precision fp32).
+         "c3p": LayerShape("c3p", 300, 300, 3, 16, 16, 4, 384, 1, 192, lr=1e-3 / 192)}
+
+
+FP32_ALU_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 TFLOP/s of FFMA at the 1965 MHz maximum SM clock
+
+
+def largest_fit_shape(base, free_bytes, frac=0.9):
+    """SURVEY.md §8(d) c5 'largest fit': the square field grid of the base field shape whose layer state fills
+    `frac` of the free HBM (cudaMemGetInfo): per field the fp32 master W~ (k x n_al), the bf16 shadow (128 x
+    n_al), b, the db partials of the two CTAs and the row scales; plus the image buffers."""
+    n_al = (base.n + 7) // 8 * 8
+    per_field = 4 * base.filters * n_al + 2 * 128 * n_al + 4 * base.n * 3 + 4 * 2 * 128 * 3 + 64
+    g = int(((frac * free_bytes) / per_field) ** 0.5)
+    while g > 1:
+        img = (g - 1) * base.stride + base.rf_h
+        img_bytes = base.batch * img * img * base.img_c * (4 * 4 + 2)   # x stage, dX (HWCN + NHWC), pf, bf16 image
+        if g * g * per_field + img_bytes <= frac * free_bytes:
+            break
+        g -= 1
+    img = (g - 1) * base.stride + base.rf_h
+    return base.replace(name=f"c5fit-{g}x{g}", img_h=img, img_w=img)
 DEVICE_INIT_PARAMS = 4e9   # above this many weights the host never materialises W (lcae_create seeds them)
 
 
@@ -318,7 +343,7 @@ def run_ours(args, shape):
         nid = obj[0]
     with torch.cuda.stream(stream):
         if True:
-            cfg = lcae.make_config(shape, precision=lcae.BF16, stream=stream.cuda_stream, world_size=world,
+            cfg = lcae.make_config(shape, precision=args.prec, stream=stream.cuda_stream, world_size=world,
                                    rank=rank, nccl_id=nid)
             L = lcae.Layer(cfg)
             if world > 1:
@@ -422,6 +447,8 @@ def run_ours(args, shape):
     if args.scaling == "weak":   # the layer grows with N: report base-layer-equivalent images/s (value x F / F_base)
         value *= shape.fields / args.base_fields
     kern_avg = kern_ms / max(1, prof_steps)   # step-kernel time per step (all its launches)
+    if kern_avg <= 0:   # the fp32 path records no step-kernel events: the whole step bounds it
+        kern_avg = ms_step
     per_kernel_flops = flops / world
     achieved = per_kernel_flops / (kern_avg * 1e-3) / 1e12
     achieved_gbs = alg_bytes(shape) / world / (kern_avg * 1e-3) / 1e9
@@ -444,7 +471,7 @@ def run_ours(args, shape):
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16" if args.prec else "f32", "data": "synthetic",
         "config": {"workload": shape.name, "image": [shape.img_h, shape.img_w, shape.img_c], "rf": shape.rf_h,
                    "stride": shape.stride, "filters": shape.filters, "pool_group": shape.pool_group,
                    "batch": shape.batch, "fields": shape.fields, "params": shape.fields * shape.filters * shape.n,
@@ -468,6 +495,14 @@ def run_ours(args, shape):
         "clocks": ck,
         "e2e": e2e,
     }
+    if not args.prec:   # the FFMA path: bound by fp32 ALU throughput (no tensor cores, several kernels per step)
+        alu_peak = FP32_ALU_TFLOPS * (ck["sm_mhz"] / ck["sm_max_mhz"] if ck.get("sm_mhz") and ck.get("sm_max_mhz") else 1)
+        ach = flops / world / (ms_step * 1e-3) / 1e12
+        line["roofline"] = {"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s",
+                            "frac": ach / alu_peak, "traffic": None, "kernel": "fp32 path (all kernels of the step)",
+                            "kernel_ms": ms_step,
+                            "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP/FFMA x SM clock "
+                                           "(median of the timed region); DESIGN.md §6"}
     if not args.no_cpu_baseline and world == 1:
         v, done, t_used, threads = cpu_oracle_rate(shape, budget_s=args.ref_budget)
         line["cpu_baseline"] = {"value": v, "unit": "images/s", "cores": threads, "kind": "oracle",
@@ -481,7 +516,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + sorted(EXTRA))
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + sorted(EXTRA) + ["c5fit"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"],
+                    help="bf16: the tcgen05 path (default); fp32: the FFMA path (needed for k > 128, e.g. c3p)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of oracle work per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -495,7 +532,14 @@ def main():
                     help="train: the training step (default); infer: encode + top-K stimuli (§8(f) item 4)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
-    shape = CONFIGS[args.config] if args.config in CONFIGS else EXTRA[args.config]
+    args.prec = 0 if args.precision == "fp32" else 1
+    if args.config == "c5fit":   # largest single-GPU layer of the c3 field shape (sized from cudaMemGetInfo)
+        import torch
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        free, _ = torch.cuda.mem_get_info()
+        shape = largest_fit_shape(CONFIGS["c3"], free)
+    else:
+        shape = CONFIGS[args.config] if args.config in CONFIGS else EXTRA[args.config]
     if args.momentum:
         shape = shape.replace(momentum=args.momentum)
     args.base_fields = shape.fields

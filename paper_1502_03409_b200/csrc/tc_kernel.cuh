@@ -112,8 +112,6 @@ struct __align__(1024) Smem {
   unsigned long long tr[48];   // optional wait-cycle / section trace (lcae_dev_trace)
 };
 
-#define UMMA_E(...) do { if (ptx::elect_one()) ptx::umma_bf16(__VA_ARGS__); __syncwarp(); } while (0)
-#define UCOMMIT_E(bar) do { if (ptx::elect_one()) ptx::umma_commit(bar); __syncwarp(); } while (0)
 
 static_assert(offsetof(Smem, bs) % 16 == 0, "float4 reads of b_f");
 static_assert(offsetof(Smem, stg) == offsetof(Smem, recv) + sizeof(Smem::recv), "recv + stg form one staging region");
@@ -398,7 +396,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     }
   } else if (warp == 1) {
     // =================================================================== MMA issuer
-    {   // warp-uniform: every lane walks the schedule, one elected lane issues (2x the single-lane MMA rate)
+    // The warp walks the schedule (waits are warp-wide); one elected lane issues each GROUP of MMAs and its
+    // commits. Descriptors are built once per operand tile and advanced by adding the byte offset >> 4 to the
+    // start-address field (smem addresses < 2^18, so the 14-bit field never carries): a handful of instructions
+    // per MMA. (The MMA warp shares an SM sub-partition with two epilogue warps: its instruction count is
+    // their issue time.)
+    {
       const uint32_t id_enc = ptx::idesc_bf16(128, KP, true, false);
       const uint32_t id_dec = ptx::idesc_bf16(128, NT, false, true);
       const uint32_t id_nx = ptx::idesc_bf16(128, NT, true, false);   // X^T (-I)
@@ -407,29 +410,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       const uint32_t id_dw2 = ptx::idesc_bf16(128, NT, true, false);
       const uint32_t id_nd = ptx::idesc_bf16(128, NT, false, false);   // delta^T (-I)
       const uint32_t sH = ptx::smem_u32(S.H), sD = ptx::smem_u32(S.D), sNI = ptx::smem_u32(S.negI);
+      // fixed-buffer descriptors
+      const uint64_t dH_k = ptx::sdesc_sw128(sH, 16, 1024);       // H' K-major (A of the decode)
+      const uint64_t dD_k = ptx::sdesc_sw128(sD, 16, 1024);       // D' K-major (A of dx)
+      const uint64_t dH_mn = ptx::sdesc_sw128(sH, 16384, 1024);   // H' as [filters x samples] (A of dW)
+      const uint64_t dD_mn = ptx::sdesc_sw128(sD, 16384, 1024);   // D' likewise
+      const uint64_t dNI = ptx::sdesc_sw128(sNI, 16, 1024);       // -I (K-major B)
+      auto adv = [](uint64_t d, uint32_t bytes) { return d + (uint64_t)(bytes >> 4); };
       uint32_t qw = 0, q0 = 0, q1 = 0, qx = 0, nf = 0, ur = 0, ud = 0, u2 = 0, qd2 = 0;
       auto wst = [&](uint32_t qq) { return ptx::smem_u32(S.Wr[qq % NW]); };
       auto wait_w = [&](uint32_t qq) {
         TWAIT(0, ptx::mbar_wait(&S.wfull[qq % NW], (qq / NW) & 1));
         ptx::tc_fence_after();
       };
-      // D = A^T W~_j: A = H' or D' (K-major [128][128]), W~_j MN-major
-      auto mma_aw = [&](uint32_t dcol, uint32_t a_base, uint32_t w_base) {
+      // D = A^T W~_j: A = H' or D' (K-major [128][128]), W~_j MN-major (elected lane only)
+      auto mma_aw = [&](uint32_t dcol, uint64_t a_desc, uint32_t w_base) {
+        const uint64_t bd = ptx::sdesc_sw128(w_base, 16384, 1024);
 #pragma unroll
-        for (int kk = 0; kk < KP / 16; ++kk) {
-          uint64_t ad = ptx::sdesc_sw128(a_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
-          uint64_t bd = ptx::sdesc_sw128(w_base + kk * 2048, 16384, 1024);
-          UMMA_E(tb + dcol, ad, bd, id_dec, kk > 0);
-        }
+        for (int kk = 0; kk < KP / 16; ++kk)
+          ptx::umma_bf16(tb + dcol, adv(a_desc, (kk >> 2) * 16384 + (kk & 3) * 32), adv(bd, kk * 2048), id_dec, kk > 0);
       };
-      // D += X_j^T (-I): subtracts the patch values exactly (X_j MN-major A, -I K-major B)
+      // D += X_j^T (-I): subtracts the patch values exactly (X_j MN-major A, -I K-major B) (elected lane only)
       auto mma_negx = [&](uint32_t dcol, uint32_t x_base) {
+        const uint64_t ad = ptx::sdesc_sw128(x_base, 8192, 1024);
 #pragma unroll
-        for (int kk = 0; kk < NT / 16; ++kk) {
-          uint64_t ad = ptx::sdesc_sw128(x_base + kk * 2048, 8192, 1024);
-          uint64_t bd = ptx::sdesc_sw128(sNI + kk * 32, 16, 1024);
-          UMMA_E(tb + dcol, ad, bd, id_nx, 1);
-        }
+        for (int kk = 0; kk < NT / 16; ++kk) ptx::umma_bf16(tb + dcol, adv(ad, kk * 2048), adv(dNI, kk * 32), id_nx, 1);
       };
       for (int fi = cid; fi < nfl; fi += ncl, ++nf) {
         // ---- pass 0: U^T = X^T W~^T (encode-only: into one of 4 U buffers, so that the next fields' encodes
@@ -444,21 +449,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           TWAIT(1, ptx::mbar_wait(&S.p0full[q0 % NP0], (q0 / NP0) & 1));
           ptx::tc_fence_after();
           ptx::fence_proxy_async_smem();
-          const uint32_t xs = ptx::smem_u32(p0slot(S, q0 % NP0));
+          if (ptx::elect_one()) {
+            const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(p0slot(S, q0 % NP0)), 8192, 1024);
+            const uint64_t bd = ptx::sdesc_sw128(wst(qw), 16, 1024);
 #pragma unroll
-          for (int kk = 0; kk < NT / 16; ++kk) {
-            uint64_t ad = ptx::sdesc_sw128(xs + kk * 2048, 8192, 1024);
-            uint64_t bd = ptx::sdesc_sw128(wst(qw) + kk * 32, 16, 1024);
-            UMMA_E(tb + ucol, ad, bd, id_enc, (j | kk) != 0);
+            for (int kk = 0; kk < NT / 16; ++kk)
+              ptx::umma_bf16(tb + ucol, adv(ad, kk * 2048), adv(bd, kk * 32), id_enc, (j | kk) != 0);
+            ptx::umma_commit(&S.wempty[qw % NW]);
+            ptx::umma_commit(&S.p0empty[q0 % NP0]);
+            if (j == T - 1) ptx::umma_commit(enc ? &S.uf[nf & 3] : &S.u_full);
           }
-          UCOMMIT_E(&S.wempty[qw % NW]);
-          UCOMMIT_E(&S.p0empty[q0 % NP0]);
+          __syncwarp();
         }
-        if (enc) {
-          UCOMMIT_E(&S.uf[nf & 3]);
-          continue;
-        }
-        UCOMMIT_E(&S.u_full);
+        if (enc) continue;
         // ---- pass 1: R_j - X_j, then G += delta_{j-GLAG} W~_{j-GLAG}^T
         TWAIT(3, ptx::mbar_wait(&S.h_ready, nf & 1));
         ptx::tc_fence_after();
@@ -469,15 +472,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           TWAIT(5, ptx::mbar_wait(&S.dl_full[db_], (ud >> 1) & 1));
           ptx::tc_fence_after();
           ptx::fence_proxy_async_smem();
-          const uint32_t dl = ptx::smem_u32(S.Dl[db_]);
+          if (ptx::elect_one()) {
+            const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(S.Dl[db_]), 16, 1024);
+            const uint64_t bd = ptx::sdesc_sw128(wst(qj), 16, 1024);
 #pragma unroll
-          for (int kk = 0; kk < NT / 16; ++kk) {
-            uint64_t ad = ptx::sdesc_sw128(dl + kk * 32, 16, 1024);
-            uint64_t bd = ptx::sdesc_sw128(wst(qj) + kk * 32, 16, 1024);
-            UMMA_E(tb + 256, ad, bd, id_g, (j | kk) != 0);
+            for (int kk = 0; kk < NT / 16; ++kk)
+              ptx::umma_bf16(tb + 256, adv(ad, kk * 32), adv(bd, kk * 32), id_g, (j | kk) != 0);
+            ptx::umma_commit(&S.dl_empty[db_]);
+            ptx::umma_commit(&S.wempty[qj % NW]);
+            if (j == T - 1) ptx::umma_commit(&S.g_full);
           }
-          UCOMMIT_E(&S.dl_empty[db_]);
-          UCOMMIT_E(&S.wempty[qj % NW]);
+          __syncwarp();
           ++ud;
         };
         for (int j = 0; j < T; ++j, ++qw, ++ur, ++q1) {
@@ -487,19 +492,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           TWAIT(44, ptx::mbar_wait(&S.p1full[s1], (q1 >> 1) & 1));
           ptx::tc_fence_after();
           ptx::fence_proxy_async_smem();
-          mma_aw(64 * rb, sH, wst(qw));
-          mma_negx(64 * rb, sD + s1 * 16384);
-          UCOMMIT_E(&S.r_full[rb]);
-          UCOMMIT_E(&S.p1empty[s1]);
-          if (step) {
-            if (j >= GLAG) issue_G(j - GLAG);
-          } else {
-            UCOMMIT_E(&S.wempty[qw % NW]);
+          if (ptx::elect_one()) {
+            mma_aw(64 * rb, dH_k, wst(qw));
+            mma_negx(64 * rb, sD + s1 * 16384);
+            ptx::umma_commit(&S.r_full[rb]);
+            ptx::umma_commit(&S.p1empty[s1]);
+            if (!step) ptx::umma_commit(&S.wempty[qw % NW]);
           }
+          __syncwarp();
+          if (step && j >= GLAG) issue_G(j - GLAG);
         }
         if (!step) continue;
         for (int j = std::max(0, T - GLAG); j < T; ++j) issue_G(j);
-        UCOMMIT_E(&S.g_full);
         // ---- pass 2 (TMEM: NB2 buffers [dX | dW] in [0,384)): delta_j is the pass-1 tile reloaded from global
         //   dx^T_j = D'^T W~_j + delta_j^T (-I)   (alpha folded into D')
         //   dW_j   = H' delta_j^T + D' X_j^T
@@ -513,35 +517,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           TWAIT(8, ptx::mbar_wait(&S.d2full[sd], (qd2 >> 1) & 1));
           TWAIT(7, ptx::mbar_wait(&S.p2_empty[pb], ((u2 / NB2) & 1) ^ 1));
           ptx::tc_fence_after();
-          mma_aw(dcol, sD, wst(qw));   // D'^T W~_j
           const uint32_t dl = ptx::smem_u32(S.Dl[sd]);
+          if (ptx::elect_one()) {
+            mma_aw(dcol, dD_k, wst(qw));   // D'^T W~_j
+            const uint64_t dlk = ptx::sdesc_sw128(dl, 16, 1024);
 #pragma unroll
-          for (int kk = 0; kk < NT / 16; ++kk) {   // + delta_j^T (-I)
-            uint64_t ad = ptx::sdesc_sw128(dl + kk * 32, 16, 1024);
-            uint64_t bd = ptx::sdesc_sw128(sNI + kk * 32, 16, 1024);
-            UMMA_E(tb + dcol, ad, bd, id_nd, 1);
-          }
-          UCOMMIT_E(&S.wempty[qw % NW]);
+            for (int kk = 0; kk < NT / 16; ++kk)   // + delta_j^T (-I)
+              ptx::umma_bf16(tb + dcol, adv(dlk, kk * 32), adv(dNI, kk * 32), id_nd, 1);
+            ptx::umma_commit(&S.wempty[qw % NW]);
+            const uint64_t dlmn = ptx::sdesc_sw128(dl, 16384, 1024);
 #pragma unroll
-          for (int kk = 0; kk < MC / 16; ++kk) {   // H' delta_j^T  (K = samples)
-            uint64_t ad = ptx::sdesc_sw128(sH + kk * 2048, 16384, 1024);
-            uint64_t bd = ptx::sdesc_sw128(dl + kk * 2048, 16384, 1024);
-            UMMA_E(tb + dcol + 64, ad, bd, id_dw1, kk > 0);
+            for (int kk = 0; kk < MC / 16; ++kk)   // H' delta_j^T  (K = samples)
+              ptx::umma_bf16(tb + dcol + 64, adv(dH_mn, kk * 2048), adv(dlmn, kk * 2048), id_dw1, kk > 0);
           }
+          __syncwarp();
           TWAIT(9, ptx::mbar_wait(&S.xfull[xsl], (qx / NX) & 1));
           ptx::tc_fence_after();
-          const uint32_t xs = ptx::smem_u32(S.Xr[xsl]);
+          if (ptx::elect_one()) {
+            const uint64_t xd = ptx::sdesc_sw128(ptx::smem_u32(S.Xr[xsl]), 16, 1024);
 #pragma unroll
-          for (int kk = 0; kk < MC / 16; ++kk) {   // + D' X_j^T
-            uint64_t ad = ptx::sdesc_sw128(sD + kk * 2048, 16384, 1024);
-            uint64_t bd = ptx::sdesc_sw128(xs + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
-            UMMA_E(tb + dcol + 64, ad, bd, id_dw2, 1);
+            for (int kk = 0; kk < MC / 16; ++kk)   // + D' X_j^T
+              ptx::umma_bf16(tb + dcol + 64, adv(dD_mn, kk * 2048), adv(xd, (kk >> 2) * 8192 + (kk & 3) * 32), id_dw2, 1);
+            ptx::umma_commit(&S.p2_full[pb]);
+            ptx::umma_commit(&S.d2empty[sd]);
+            ptx::umma_commit(&S.xempty[xsl]);
+            if (j == T - 1) ptx::umma_commit(&S.p0_ok);   // D', delta and the X ring are free for the next field
           }
-          UCOMMIT_E(&S.p2_full[pb]);
-          UCOMMIT_E(&S.d2empty[sd]);
-          UCOMMIT_E(&S.xempty[xsl]);
+          __syncwarp();
         }
-        UCOMMIT_E(&S.p0_ok);   // D', delta and the X ring are free for the next field's pass 0
       }
     }
     __syncwarp();
@@ -764,6 +767,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           isgr[i] = S.isig[r];
         }
 #pragma unroll 1
+        // dX piece words of the warp's two 16-column rounds, loaded one tile ahead (an L2 round trip: the 227 KB
+        // shared-memory carve-out leaves L1 too small to keep the table resident)
+        auto piece_words = [&](int jj, uint32_t &a0, uint32_t &a1) {
+          const uint32_t *dxp = P.dxpieces + ((size_t)jj * 4 + 2 * half) * DXPMAX;
+          a0 = lane < DXPMAX ? __ldg(dxp + lane) : 0xFFFFFFFFu;
+          a1 = lane < DXPMAX ? __ldg(dxp + DXPMAX + lane) : 0xFFFFFFFFu;
+        };
+        uint32_t pwn0, pwn1;
+        piece_words(0, pwn0, pwn1);
         for (int j = 0; j < T; ++j, ++u2) {
           const uint32_t pb = u2 % NB2, base = 128 * pb;
           TWAIT(18, ptx::mbar_wait(&S.p2_full[pb], (u2 / NB2) & 1));
@@ -776,9 +788,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           // TMA unit: each 16-column round is staged in this warp's slice as [16 patch rows][32 samples] (one
           // conflict-free 128-byte row per column) and reduce-added (cp.reduce.async.bulk.tensor .add.f32) in boxes
           // of consecutive image rows from the host piece table (lanes 0..15 issue one piece each).
-          const uint32_t *dxp = P.dxpieces + ((size_t)j * 4 + 2 * half) * DXPMAX;
-          const uint32_t pw0 = lane < DXPMAX ? __ldg(dxp + lane) : 0xFFFFFFFFu;
-          const uint32_t pw1 = lane < DXPMAX ? __ldg(dxp + DXPMAX + lane) : 0xFFFFFFFFu;
+          const uint32_t pw0 = pwn0, pw1 = pwn1;
+          if (j + 1 < T) piece_words(j + 1, pwn0, pwn1);
           float xv[32];
           auto dx_round = [&](auto RI, uint32_t pw) {
             constexpr int r = decltype(RI)::value;
