@@ -304,12 +304,13 @@ EXTRA = {"c15b": LayerShape("c15b", 710, 712, 3, 18, 18, 2, 128, 1, 256, lr=1e-3
 FP32_ALU_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 TFLOP/s of FFMA at the 1965 MHz maximum SM clock
 
 
-def largest_fit_shape(base, free_bytes, frac=0.9):
+def largest_fit_shape(base, free_bytes, frac=0.88):
     """SURVEY.md §8(d) c5 'largest fit': the square field grid of the base field shape whose layer state fills
     `frac` of the free HBM (cudaMemGetInfo): per field the fp32 master W~ (k x n_al), the bf16 shadow (128 x
     n_al), b, the db partials of the two CTAs and the row scales; plus the image buffers."""
     n_al = (base.n + 7) // 8 * 8
-    per_field = 4 * base.filters * n_al + 2 * 128 * n_al + 4 * base.n * 3 + 4 * 2 * 128 * 3 + 64
+    per_field = (4 * base.filters * n_al + 2 * 128 * n_al + 4 * base.n * 3 + 4 * 2 * 128 * 4 + 4 * base.filters * 3
+                 + 128)   # W~, shadow, b + 2 db partials, row-sum partials, sigma + rowsq, loss / alpha partials
     g = int(((frac * free_bytes) / per_field) ** 0.5)
     while g > 1:
         img = (g - 1) * base.stride + base.rf_h

@@ -159,6 +159,11 @@ lcae_status lcae_set_params(lcae_layer *L, const float *W, const float *alpha, c
 /* Copy the current parameters out (host or device pointers; NULL skips). */
 lcae_status lcae_get_params(lcae_layer *L, float *W, float *alpha, float *b);
 
+/* The parameters of fields [f0, f0 + count) only (canonical layouts restricted to the range; host or device;
+ * NULL skips): sampled checks of layers too large to copy out whole (e.g. the 15 B-weight point).
+ * Errors: ARG (range outside the layer), CUDA. */
+lcae_status lcae_get_field_params(lcae_layer *L, int64_t f0, int64_t count, float *W, float *alpha, float *b);
+
 /* Gradients of the most recent lcae_step, taken at the pre-update parameters (requires keep_grads=1,
  * else LCAE_ERR_CONFIG). dW [F][k][n], dalpha [F], db [F][n]; host or device; NULL skips. */
 lcae_status lcae_get_grads(lcae_layer *L, float *dW, float *dalpha, float *db);

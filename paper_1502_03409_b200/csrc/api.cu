@@ -272,7 +272,8 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
   CKF(dmalloc(L, &L->x_stage, m * img * 4));   // >= the owned pixels of a model-parallel rank
   CKF(dmalloc(L, &L->dxt, mp * img * 4));
   CKF(dmalloc(L, &L->dx_nhwc, m * img * 4));
-  CKF(dmalloc(L, &L->pooled, m * F * (k / g.g) * 4));
+  // the pooled-code buffer (m F k/g floats, 128 KB per c3 field) is allocated on the first forward / encode that
+  // asks for it: a training-only layer leaves that HBM to its weights (the largest-fit point)
   CKF(dmalloc(L, &L->loss_part, F * 2 * sizeof(double)));
   CKF(dmalloc(L, &L->loss_dev, 2 * sizeof(double)));
   CKF(cudaMemsetAsync(L->loss_dev, 0, 2 * sizeof(double), L->st));
@@ -352,6 +353,26 @@ lcae_status lcae_get_params(lcae_layer *L, float *W, float *alpha, float *b) {
   return LCAE_OK;
 }
 
+lcae_status lcae_get_field_params(lcae_layer *L, int64_t f0, int64_t count, float *W, float *alpha, float *b) {
+  if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
+  const Geo &g = L->geo;
+  if (f0 < 0 || count < 0 || f0 + count > g.F) { set_error("lcae_get_field_params: field range outside the layer"); return LCAE_ERR_ARG; }
+  if (!count) return LCAE_OK;
+  lcae_status s;
+  if (W) {   // sigma (.) W~ of the range, through a device staging buffer
+    const size_t bytes = (size_t)count * g.k * g.n * 4;
+    float *tmp = nullptr;
+    LCAE_CK(cudaMallocAsync(&tmp, bytes, L->st));
+    if ((s = launch_get_W_range(L, tmp, f0, count))) return s;
+    LCAE_CK(cudaMemcpyAsync(W, tmp, bytes, cudaMemcpyDefault, L->st));
+    LCAE_CK(cudaFreeAsync(tmp, L->st));
+  }
+  if (alpha && (s = copy_any(L, alpha, L->alpha + f0, (size_t)count * 4))) return s;
+  if (b && (s = copy_any(L, b, L->b + f0 * g.n, (size_t)count * g.n * 4))) return s;
+  LCAE_CK(cudaStreamSynchronize(L->st));
+  return LCAE_OK;
+}
+
 lcae_status lcae_get_grads(lcae_layer *L, float *dW, float *dalpha, float *db) {
   if (!L) { set_error("NULL handle"); return LCAE_ERR_ARG; }
   if (!L->cfg.keep_grads) return config_error("lcae_get_grads needs keep_grads = 1");
@@ -377,6 +398,7 @@ static lcae_status run(lcae_layer *L, const float *x, bool update, float *dx, fl
     set_error("model-parallel test-mode layer (nccl_id == NULL): drive it with lcae_mp_phase");
     return LCAE_ERR_ARG;
   }
+  if (pooled && !L->pooled) LCAE_CK(dmalloc(L, &L->pooled, (size_t)g.m * g.F * (g.k / g.g) * 4));
   if ((s = stage_input(L, x))) return s;
   if (L->mpst) {   // model parallel (mp.cu): halo exchange, interior / boundary fields, dX return, loss all-reduce
     if (encode_only) { set_error("lcae_encode is not available on a model-parallel layer"); return LCAE_ERR_ARG; }
@@ -457,6 +479,7 @@ lcae_status lcae_mp_phase(lcae_layer *L, int32_t phase, int32_t update, const fl
     L->launches = 0;
     if ((s = stage_input(L, x))) return s;
   }
+  if (pooled && !L->pooled) LCAE_CK(dmalloc(L, &L->pooled, (size_t)L->geo.m * L->geo.F * (L->geo.k / L->geo.g) * 4));
   if ((s = mp_phase(L, phase, update != 0, pooled != nullptr))) return s;
   if (phase == 2) {
     if (update) {

@@ -165,9 +165,9 @@ __global__ void fill_f32(float *p, int64_t n, float v) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) p[t] = v;
 }
 
-// W_out[f][j][t] = sigma[f][j] * W~[f][j][t]
-__global__ void get_w(Geo g, int wp, const float *W, const float *sigma, float *out) {
-  const int64_t tot = (int64_t)g.F * g.k * g.n;
+// W_out[f][j][t] = sigma[f][j] * W~[f][j][t] for fields [f0, f0 + nf) (W, sigma already offset to f0)
+__global__ void get_w(Geo g, int wp, const float *W, const float *sigma, float *out, int64_t nf) {
+  const int64_t tot = nf * g.k * g.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = t / g.n;
     out[t] = W[row * wp + (t - row * g.n)] * sigma[row];
@@ -264,7 +264,14 @@ lcae_status launch_fill(lcae_layer *L, float *p, int64_t n, float v) {
 }
 
 lcae_status launch_get_W(lcae_layer *L, float *Wout) {
-  get_w<<<L->sm_count * 8, 256, 0, L->st>>>(L->geo, L->wp, L->W, L->sigma, Wout);
+  get_w<<<L->sm_count * 8, 256, 0, L->st>>>(L->geo, L->wp, L->W, L->sigma, Wout, L->geo.F);
+  LCAE_CK_LAUNCH(L);
+  return LCAE_OK;
+}
+
+lcae_status launch_get_W_range(lcae_layer *L, float *Wout, int64_t f0, int64_t nf) {
+  const Geo &g = L->geo;
+  get_w<<<L->sm_count * 8, 256, 0, L->st>>>(g, L->wp, L->W + f0 * g.k * L->wp, L->sigma + f0 * g.k, Wout, nf);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }

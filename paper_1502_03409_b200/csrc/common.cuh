@@ -212,6 +212,7 @@ lcae_status launch_loss_reduce(lcae_layer *L, bool update);
 lcae_status launch_init_params(lcae_layer *L);
 lcae_status launch_fill(lcae_layer *L, float *p, int64_t n, float v);
 lcae_status launch_get_W(lcae_layer *L, float *Wout);   // sigma (.) W~ -> dense [F][k][n]
+lcae_status launch_get_W_range(lcae_layer *L, float *Wout, int64_t f0, int64_t nf);
 lcae_status launch_refresh_shadow(lcae_layer *L);       // W~ -> bf16 shadow
 
 }  // namespace lcae

@@ -109,7 +109,7 @@ struct __align__(1024) Smem {
   uint64_t recv_full[NEPI], peer_free[NEPI];   // per epilogue warp: the dW exchange couples warp w of the two
                                                // CTAs only (not all 16 warps of the pair)
   uint32_t tmem_base;
-  unsigned long long tr[48];   // optional wait-cycle / section trace (lcae_dev_trace)
+  unsigned long long tr[64];   // optional wait-cycle / section trace (lcae_dev_trace); [48+w]/[56+w]: per epilogue warp
 };
 
 
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
   } while (0)
 
   // ---- one-time setup
-  if (threadIdx.x < 48) S.tr[threadIdx.x] = 0ull;
+  if (threadIdx.x < 64) S.tr[threadIdx.x] = 0ull;
   long long tmark = 0;
 #define TMARK(IDX)                                                                               \
   do {                                                                                           \
@@ -668,7 +668,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       for (int j = 0; j < (enc ? 0 : T); ++j, ++ur) {
         const uint32_t rb = ur % NRB;
         if (j == 0) TWAIT(43, ptx::mbar_wait(&S.r_full[rb], (ur / NRB) & 1));
-        else TWAIT(12, ptx::mbar_wait(&S.r_full[rb], (ur / NRB) & 1));
+        else {
+          const long long tw0 = TR ? clock64() : 0;
+          TWAIT(12, ptx::mbar_wait(&S.r_full[rb], (ur / NRB) & 1));
+          if (TR && P.trace && lane == 0) atomicAdd(&S.tr[56 + ew], (unsigned long long)(clock64() - tw0));
+        }
         ptx::tc_fence_after();
         float rv[32];
         ptx::tmem_ld16(tl + 64 * rb + hc, rv);
@@ -778,7 +782,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         piece_words(0, pwn0, pwn1);
         for (int j = 0; j < T; ++j, ++u2) {
           const uint32_t pb = u2 % NB2, base = 128 * pb;
-          TWAIT(18, ptx::mbar_wait(&S.p2_full[pb], (u2 / NB2) & 1));
+          {
+            const long long tw0 = TR ? clock64() : 0;
+            TWAIT(18, ptx::mbar_wait(&S.p2_full[pb], (u2 / NB2) & 1));
+            if (TR && P.trace && lane == 0) atomicAdd(&S.tr[48 + ew], (unsigned long long)(clock64() - tw0));
+          }
           ptx::tc_fence_after();
           TMARK(35);
           const int swr = (lane >> 1) & 3;                     // swizzle of this lane's row (row = lane)
@@ -999,7 +1007,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
                       (unsigned long long)(clock64() - t_start));
   ptx::tc_fence_before();
   __syncthreads();
-  if (P.trace && threadIdx.x < 48) atomicAdd(&P.trace[threadIdx.x], S.tr[threadIdx.x]);
+  if (P.trace && threadIdx.x < 64) atomicAdd(&P.trace[threadIdx.x], S.tr[threadIdx.x]);
 #undef TWAIT
 #undef TMARK
   if (CB > 1) ptx::cluster_sync();

@@ -57,6 +57,7 @@ def _load():
         "lcae_set_params": (C.c_int, [P, P, P, P]),
         "lcae_get_params": (C.c_int, [P, P, P, P]),
         "lcae_get_grads": (C.c_int, [P, P, P, P]),
+        "lcae_get_field_params": (C.c_int, [P, C.c_int64, C.c_int64, P, P, P]),
         "lcae_forward": (C.c_int, [P, P, P, C.POINTER(C.c_double)]),
         "lcae_step": (C.c_int, [P, P, P, C.POINTER(C.c_double)]),
         "lcae_encode": (C.c_int, [P, P, P, C.POINTER(C.c_double)]),
@@ -94,7 +95,7 @@ lib = _load()
 
 # Every symbol include/lcae.h declares (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("lcae_config_default", "lcae_geometry", "lcae_create", "lcae_destroy", "lcae_set_params",
-               "lcae_get_params", "lcae_get_grads", "lcae_forward", "lcae_encode", "lcae_step", "lcae_last_loss",
+               "lcae_get_params", "lcae_get_grads", "lcae_get_field_params", "lcae_forward", "lcae_encode", "lcae_step", "lcae_last_loss",
                "lcae_sync", "lcae_field_losses", "lcae_nccl_unique_id", "lcae_mp_phase", "lcae_mp_buffer",
                "lcae_mp_fields",
                "lcae_topk_init", "lcae_topk_update", "lcae_lcn", "lcae_prefetch_input",
@@ -201,6 +202,10 @@ class Layer:
 
     def get_params(self, W=None, alpha=None, b=None):
         check(lib.lcae_get_params(self.h, _ptr(W), _ptr(alpha), _ptr(b)))
+
+    def get_field_params(self, f0, count, W=None, alpha=None, b=None):
+        """Parameters of fields [f0, f0 + count) (lcae_get_field_params)."""
+        check(lib.lcae_get_field_params(self.h, f0, count, _ptr(W), _ptr(alpha), _ptr(b)))
 
     def get_grads(self, dW=None, dalpha=None, db=None):
         check(lib.lcae_get_grads(self.h, _ptr(dW), _ptr(dalpha), _ptr(db)))

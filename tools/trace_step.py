@@ -49,7 +49,7 @@ for _ in range(steps):
     run()
 torch.cuda.synchronize()
 ms, nl = L.profile_read()
-out = (C.c_ulonglong * 48)()
+out = (C.c_ulonglong * 64)()
 lcae.check(lib.lcae_dev_trace(L.h, 0, out))
 ctas = min(shape.fields * ((shape.batch + 127) // 128), 148 // ((shape.batch + 127) // 128) * ((shape.batch + 127) // 128))
 per = lambda v: v / ctas / steps  # noqa: E731
@@ -58,3 +58,6 @@ print(f"{cfg_name}: kernel {ms / nl:.3f} ms/launch; per-CTA cycles per step (mma
 for i in sorted(NAMES):
     if out[i]:
         print(f"  {NAMES[i]:20s} {per(out[i]):14.0f}  {100 * per(out[i]) / tot:6.1f}%")
+print("  per epilogue warp (warp = 2 + w, TMEM quarter w % 4, column half w // 4): wait p2_full / wait r_full")
+for w in range(8):
+    print(f"    w{w} (warp {w + 2}, SMSP {(w + 2) % 4}): {100 * per(out[48 + w]) / tot:5.1f}%  {100 * per(out[56 + w]) / tot:5.1f}%")
