@@ -173,14 +173,19 @@ def run_reference(args, shape):
         v, done, t_used, threads = cpu_oracle_rate(shape, budget_s=per)
         steps.append((v, done, t_used))
     v = statistics.median(s[0] for s in steps)
+    frac = statistics.median(s[1] for s in steps) / shape.fields
     sample = (f"{steps[0][1]} of {shape.fields} fields per step (stratified), extrapolated linearly; "
               f"fp64 numpy oracle, {steps[0][2]:.1f} s per sample")
+    # a "step" of this arm is one bounded sample (a fraction `sample_fraction` of the layer's fields): ms_per_step is
+    # its measured time, so steps x ms_per_step is the arm's wall time; value = m x fraction / sample time = the
+    # images/s of the whole layer at the oracle's per-field cost (every field costs the same)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "images/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * shape.batch / v,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * shape.batch * frac / v,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": shape.name, "image": [shape.img_h, shape.img_w, shape.img_c],
                        "rf": shape.rf_h, "stride": shape.stride, "filters": shape.filters,
-                       "pool_group": shape.pool_group, "batch": shape.batch, "fields": shape.fields},
+                       "pool_group": shape.pool_group, "batch": shape.batch, "fields": shape.fields,
+                       "sample_fraction": frac},
             "cpu_baseline": {"value": v, "unit": "images/s", "cores": threads, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -524,6 +529,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of oracle work per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--momentum", type=float, default=0.0, help="SGD momentum (SURVEY.md §8(f) item 3: 0.9)")
+    ap.add_argument("--batch", type=int, default=0, help="override the config's mini-batch (PAPER.md:111: 192)")
     ap.add_argument("--graph", action="store_true", help="replay each step from a captured CUDA graph (1 GPU)")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: the config's layer on N GPUs (default); weak: the field grid grows with N "
@@ -543,6 +549,8 @@ def main():
         shape = CONFIGS[args.config] if args.config in CONFIGS else EXTRA[args.config]
     if args.momentum:
         shape = shape.replace(momentum=args.momentum)
+    if args.batch:
+        shape = shape.replace(name=f"{shape.name}-m{args.batch}", batch=args.batch, lr=1e-3 / args.batch)
     args.base_fields = shape.fields
     if args.scaling == "weak":
         from paper_1502_03409_b200.parallel import factor
