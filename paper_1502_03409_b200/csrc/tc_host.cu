@@ -161,8 +161,8 @@ lcae_status tc_alloc(lcae_layer *L) {
   LCAE_CK(dmalloc(L, &s->rowsq_part, (size_t)g.F * s->CB * 2 * tc::KP * 4));
   LCAE_CK(dmalloc(L, &s->dbscr, (size_t)s->grid * 4 * tc::MAX_NPAD * 4));   // per-CTA db partials (L2)
   LCAE_CK(dmalloc(L, &s->dscr, (size_t)s->grid * T * 16384));   // per-CTA pass-1 delta tiles (L2-resident)
-  LCAE_CK(dmalloc(L, &s->trace, 64 * sizeof(unsigned long long)));
-  LCAE_CK(cudaMemset(s->trace, 0, 64 * sizeof(unsigned long long)));
+  LCAE_CK(dmalloc(L, &s->trace, (64 + 256) * sizeof(unsigned long long)));
+  LCAE_CK(cudaMemset(s->trace, 0, (64 + 256) * sizeof(unsigned long long)));
   // Wb is [F][KP][n_al] (pad rows zero) for the bf16 path
   cudaFree(L->Wb);
   LCAE_CK(dmalloc(L, &L->Wb, (size_t)g.F * tc::KP * L->n_al * 2));
@@ -326,8 +326,8 @@ extern "C" lcae_status lcae_dev_trace(lcae_layer *L, int enable, unsigned long l
   if (!L || !L->tc) { set_error("lcae_dev_trace: bf16 layer required"); return LCAE_ERR_ARG; }
   if (out32) {
     LCAE_CK(cudaStreamSynchronize(L->st));
-    LCAE_CK(cudaMemcpy(out32, L->tc->trace, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    LCAE_CK(cudaMemset(L->tc->trace, 0, 64 * sizeof(unsigned long long)));
+    LCAE_CK(cudaMemcpy(out32, L->tc->trace, (64 + 256) * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    LCAE_CK(cudaMemset(L->tc->trace, 0, (64 + 256) * sizeof(unsigned long long)));
   }
   L->tc->trace_on = enable ? 1 : 0;
   return LCAE_OK;

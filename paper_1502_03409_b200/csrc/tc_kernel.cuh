@@ -39,7 +39,8 @@ namespace tc {
 constexpr int KP = 128;        // filters padded to one TMEM lane block
 constexpr int NT = 64;         // n-tile
 constexpr int MC = 128;        // samples per CTA
-constexpr int NW = 3;          // W ring stages
+constexpr int NW = 4;          // W ring stages (pass 1 holds W~_j from R_j until G_j: 4 stages give the
+                               // ~2 us L2 -> smem TMA latency a tile of slack)
 constexpr int NX = 2;          // pass-2 X ring stages
 constexpr int NP0 = 8;         // pass-0 X ring slots (D'[0..1], delta[0..1], pass-2 X ring [0..1], H'[0..1])
 constexpr int NRB = 4;         // pass-1 R buffers
@@ -91,17 +92,17 @@ struct __align__(1024) Smem {
   uint8_t H[32768];
   uint8_t D[32768];          // pass 0: X slots 0,1; pass 1: X ring
   uint8_t Dl[2][16384];      // pass 0: X slots 2,3
-  uint8_t negI[8192];        // -I (64 x 64 bf16, SW128)
-  float recv[2][128][16];    // peer's dW partial for this CTA's owned 16-column chunks, [half][row][col]
+  uint8_t negI[2048];        // -I_16 (16 x 16 bf16, SW128 rows): the -x / -delta MMAs run as 4 N = 16 blocks
+  uint32_t recv[2][128][8];  // peer's dW partial for this CTA's owned 16-column chunks, [half][row][16 bf16] (R25)
   float stg[NEPI][32][16];   // per-warp 2 KB staging: the own dW chunk's transpose (16-byte chunks swizzled), then
-                             // the dX rounds ([16 patch rows][32 samples], the TMA reduce-add source);
-                             // forward / encode modes: recv + stg (contiguous) = 8 x 4 KB pooled-output staging
-  float bs[MAX_NPAD];        // b_f of the current field (epilogue)
+                             // the dX rounds ([16 patch rows][32 samples], the TMA reduce-add source); during
+                             // E0 / E1 of a training step the first 4 KB hold b_f (all warps), in forward / encode
+                             // the pooled-output staging
   float sig[KP];
   float isig[KP];            // 1 / sig
   double redd[NEPI][2];
   float redf[NEPI];
-  uint64_t wfull[NW], wempty[NW], xfull[NX], xempty[NX], p0full[NP0], p0empty[NP0], p1full[2], p1empty[2];
+  uint64_t wfull[NW], wempty[NW], xfull[NX], xempty[NX], p0full[NP0], p0empty[NP0], p1full[4], p1empty[4];
   uint64_t p0_ok, u_full, h_ready, g_full, d_ready, d_stored;
   uint64_t uf[4], ue[4];     // encode-only mode: 4 U buffers in TMEM (full / free)
   uint64_t r_full[NRB], r_empty[NRB], dl_full[2], dl_empty[2];
@@ -113,8 +114,13 @@ struct __align__(1024) Smem {
 };
 
 
-static_assert(offsetof(Smem, bs) % 16 == 0, "float4 reads of b_f");
-static_assert(offsetof(Smem, stg) == offsetof(Smem, recv) + sizeof(Smem::recv), "recv + stg form one staging region");
+static_assert(offsetof(Smem, stg) % 16 == 0, "float4 reads of b_f");
+static_assert(sizeof(Smem::stg) >= MAX_NPAD * sizeof(float), "b_f fits the staging slices");
+
+// pass 1's X ring: the D' buffer (2 slots) and, in a training step, the pass-2 X ring too (idle from the end of
+// pass 0 to the start of pass 2): 4 slots, so the X tiles arrive ahead of the R MMAs despite ~2 us of L2 -> smem
+// TMA latency (measured with the traced variant's timeline)
+__device__ __forceinline__ uint8_t *p1slot(Smem &S, uint32_t i) { return i < 2 ? S.D + i * 16384 : S.Xr[i - 2]; }
 
 // pass 0 borrows every operand buffer the previous field's pass 2 is done with (all free at p0_ok)
 __device__ __forceinline__ uint8_t *p0slot(Smem &S, int i) {
@@ -138,10 +144,10 @@ __device__ __forceinline__ void red_v4(float *p, float a, float b, float c, floa
 }
 
 // e = (R - x) + b over this warp's 32 columns of a tile for this thread's sample; rv <- delta = 2e (masked).
-__device__ __forceinline__ float residual32(float (&rv)[32], int c0, int n, const float *bf_, bool svalid) {
+__device__ __forceinline__ float residual32(float (&rv)[32], int c0, int n, const float *bf_, bool svalid, bool b16) {
   float jr = 0.f;
   const float4 *b4 = reinterpret_cast<const float4 *>(bf_ + c0);   // c0 % 32 == 0: 16-byte aligned broadcasts
-  if (svalid && c0 + 32 <= n) {   // full run (all but the ragged last tile): no masking
+  if (svalid && c0 + 32 <= n && b16) {   // full run (all but the ragged last tile): no masking
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const float4 bv = b4[q];
@@ -158,7 +164,7 @@ __device__ __forceinline__ float residual32(float (&rv)[32], int c0, int n, cons
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
     const int nn = c0 + c;
-    float e = rv[c] + bf_[nn];   // entries of bs past n are never initialised: selected away below
+    float e = rv[c] + (nn < n ? bf_[nn] : 0.f);
     e = (svalid && nn < n) ? e : 0.f;
     jr = fmaf(e, e, jr);
     rv[c] = 2.f * e;
@@ -198,6 +204,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     LCAE_DCHECK(f_ >= 0 && f_ < P.g.F);
     return f_;
   };
+  const uint32_t np1 = step ? 4u : 2u;   // pass-1 X ring slots (p1slot)
   const int64_t prow = (int64_t)P.g.H * P.g.W * P.g.C;   // pixel-feature rows of the HWCN image (checked build)
   (void)prow;
   // trace: lane 0 of the producers / MMA warp and of epilogue warp 2 record their barrier-wait cycles
@@ -214,6 +221,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     }                                                                                            \
   } while (0)
 
+  // timeline (traced variant only): clock64 of pipeline events of CTA 0's third field, into P.trace[64 + id]
+#define TLOG(ID, NF)                                                                             \
+  do {                                                                                           \
+    if (TR && P.trace && blockIdx.x == 0 && (NF) == 2 && lane == 0)                             \
+      P.trace[64 + (ID)] = (unsigned long long)clock64();                                        \
+  } while (0)
   // ---- one-time setup
   if (threadIdx.x < 64) S.tr[threadIdx.x] = 0ull;
   long long tmark = 0;
@@ -231,7 +244,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     for (int t = threadIdx.x; t < (int)(sizeof(S.Xr) + sizeof(S.H) + sizeof(S.D) + sizeof(S.Dl)) / 16; t += NTHREADS)
       z[t] = make_uint4(0, 0, 0, 0);
   }
-  for (int t = threadIdx.x; t < 64 * 64; t += NTHREADS) {
+  for (int t = threadIdx.x; t < 16 * 64; t += NTHREADS) {   // rows 0..15 of a SW128 K-major tile; K 0..15 used
     const int r = t >> 6, c = t & 63;
     *reinterpret_cast<__nv_bfloat16 *>(S.negI + ptx::sw128_off(r, c)) = __float2bfloat16_rn(r == c ? -1.f : 0.f);
   }
@@ -239,7 +252,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     for (int i = 0; i < NW; ++i) { ptx::mbar_init(&S.wfull[i], 1); ptx::mbar_init(&S.wempty[i], 1); }
     for (int i = 0; i < NX; ++i) { ptx::mbar_init(&S.xfull[i], 1); ptx::mbar_init(&S.xempty[i], 1); }
     for (int i = 0; i < NP0; ++i) { ptx::mbar_init(&S.p0full[i], 1); ptx::mbar_init(&S.p0empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { ptx::mbar_init(&S.p1full[i], 1); ptx::mbar_init(&S.p1empty[i], 1); }
+    for (int i = 0; i < 4; ++i) { ptx::mbar_init(&S.p1full[i], 1); ptx::mbar_init(&S.p1empty[i], 1); }
     ptx::mbar_init(&S.p0_ok, 1);
     for (int i = 0; i < NB2; ++i) { ptx::mbar_init(&S.p2_full[i], 1); ptx::mbar_init(&S.p2_empty[i], NEPI); }
     ptx::mbar_init(&S.u_full, 1);
@@ -354,13 +367,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       // pass 1 ring lives in the D' buffer once the encode MMAs are done
       TWAIT(30, ptx::mbar_wait(&S.u_full, nf & 1));
       for (int j = 0; j < T; ++j, ++q1) {
-        const int s = q1 & 1;
-        TWAIT(30, ptx::mbar_wait(&S.p1empty[s], ((q1 >> 1) & 1) ^ 1));
-        load_tile(S.D + s * 16384, &S.p1full[s], j);
+        const uint32_t s = q1 % np1;
+        TWAIT(30, ptx::mbar_wait(&S.p1empty[s], ((q1 / np1) & 1) ^ 1));
+        load_tile(p1slot(S, s), &S.p1full[s], j);
       }
       if (!step) {   // forward: the next field's pass 0 reuses D'; wait until both slots were consumed
-        for (uint32_t qq = q1 - std::min<uint32_t>(q1, 2); qq < q1; ++qq)
-          ptx::mbar_wait(&S.p1empty[qq & 1], (qq >> 1) & 1);
+        for (uint32_t qq = q1 - std::min<uint32_t>(q1, np1); qq < q1; ++qq)
+          ptx::mbar_wait(&S.p1empty[qq % np1], (qq / np1) & 1);
         continue;
       }
       // pass 2: delta_j (the pass-1 images, once all are stored and the G MMAs are done with the ring) and X_j
@@ -404,11 +417,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     {
       const uint32_t id_enc = ptx::idesc_bf16(128, KP, true, false);
       const uint32_t id_dec = ptx::idesc_bf16(128, NT, false, true);
-      const uint32_t id_nx = ptx::idesc_bf16(128, NT, true, false);   // X^T (-I)
+      const uint32_t id_nx = ptx::idesc_bf16(128, 16, true, false);   // X^T (-I_16), per 16-column block
       const uint32_t id_g = ptx::idesc_bf16(128, KP, false, false);
       const uint32_t id_dw1 = ptx::idesc_bf16(128, NT, true, true);
       const uint32_t id_dw2 = ptx::idesc_bf16(128, NT, true, false);
-      const uint32_t id_nd = ptx::idesc_bf16(128, NT, false, false);   // delta^T (-I)
+      const uint32_t id_nd = ptx::idesc_bf16(128, 16, false, false);   // delta^T (-I_16), per 16-column block
       const uint32_t sH = ptx::smem_u32(S.H), sD = ptx::smem_u32(S.D), sNI = ptx::smem_u32(S.negI);
       // fixed-buffer descriptors
       const uint64_t dH_k = ptx::sdesc_sw128(sH, 16, 1024);       // H' K-major (A of the decode)
@@ -430,11 +443,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         for (int kk = 0; kk < KP / 16; ++kk)
           ptx::umma_bf16(tb + dcol, adv(a_desc, (kk >> 2) * 16384 + (kk & 3) * 32), adv(bd, kk * 2048), id_dec, kk > 0);
       };
-      // D += X_j^T (-I): subtracts the patch values exactly (X_j MN-major A, -I K-major B) (elected lane only)
+      // D += X_j^T (-I): subtracts the patch values exactly (X_j MN-major A, -I K-major B): columns 16kk..+16 of D
+      // take K rows 16kk..+16 of X_j^T times -I_16 (elected lane only)
       auto mma_negx = [&](uint32_t dcol, uint32_t x_base) {
         const uint64_t ad = ptx::sdesc_sw128(x_base, 8192, 1024);
 #pragma unroll
-        for (int kk = 0; kk < NT / 16; ++kk) ptx::umma_bf16(tb + dcol, adv(ad, kk * 2048), adv(dNI, kk * 32), id_nx, 1);
+        for (int kk = 0; kk < NT / 16; ++kk) ptx::umma_bf16(tb + dcol + 16 * kk, adv(ad, kk * 2048), dNI, id_nx, 1);
       };
       for (int fi = cid; fi < nfl; fi += ncl, ++nf) {
         // ---- pass 0: U^T = X^T W~^T (encode-only: into one of 4 U buffers, so that the next fields' encodes
@@ -483,23 +497,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             if (j == T - 1) ptx::umma_commit(&S.g_full);
           }
           __syncwarp();
+          TLOG(16 + j, nf);
           ++ud;
         };
         for (int j = 0; j < T; ++j, ++qw, ++ur, ++q1) {
           wait_w(qw);
-          const uint32_t rb = ur % NRB, s1 = q1 & 1;
+          TLOG(80 + j, nf);
+          const uint32_t rb = ur % NRB, s1 = q1 % np1;
           TWAIT(4, ptx::mbar_wait(&S.r_empty[rb], ((ur / NRB) & 1) ^ 1));
-          TWAIT(44, ptx::mbar_wait(&S.p1full[s1], (q1 >> 1) & 1));
+          TWAIT(44, ptx::mbar_wait(&S.p1full[s1], (q1 / np1) & 1));
+          TLOG(64 + j, nf);
           ptx::tc_fence_after();
           ptx::fence_proxy_async_smem();
           if (ptx::elect_one()) {
             mma_aw(64 * rb, dH_k, wst(qw));
-            mma_negx(64 * rb, sD + s1 * 16384);
+            mma_negx(64 * rb, ptx::smem_u32(p1slot(S, s1)));
             ptx::umma_commit(&S.r_full[rb]);
             ptx::umma_commit(&S.p1empty[s1]);
             if (!step) ptx::umma_commit(&S.wempty[qw % NW]);
           }
           __syncwarp();
+          TLOG(0 + j, nf);
           if (step && j >= GLAG) issue_G(j - GLAG);
         }
         if (!step) continue;
@@ -514,16 +532,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           const uint32_t pb = u2 % NB2, xsl = qx % NX, sd = qd2 & 1;
           const uint32_t dcol = 128 * pb;
           wait_w(qw);
+          TLOG(176 + j, nf);
           TWAIT(8, ptx::mbar_wait(&S.d2full[sd], (qd2 >> 1) & 1));
+          TLOG(160 + j, nf);
           TWAIT(7, ptx::mbar_wait(&S.p2_empty[pb], ((u2 / NB2) & 1) ^ 1));
+          TLOG(192 + j, nf);
           ptx::tc_fence_after();
           const uint32_t dl = ptx::smem_u32(S.Dl[sd]);
           if (ptx::elect_one()) {
             mma_aw(dcol, dD_k, wst(qw));   // D'^T W~_j
             const uint64_t dlk = ptx::sdesc_sw128(dl, 16, 1024);
 #pragma unroll
-            for (int kk = 0; kk < NT / 16; ++kk)   // + delta_j^T (-I)
-              ptx::umma_bf16(tb + dcol, adv(dlk, kk * 32), adv(dNI, kk * 32), id_nd, 1);
+            for (int kk = 0; kk < NT / 16; ++kk)   // + delta_j^T (-I): 16-column blocks
+              ptx::umma_bf16(tb + dcol + 16 * kk, adv(dlk, kk * 32), dNI, id_nd, 1);
             ptx::umma_commit(&S.wempty[qw % NW]);
             const uint64_t dlmn = ptx::sdesc_sw128(dl, 16384, 1024);
 #pragma unroll
@@ -532,6 +553,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           }
           __syncwarp();
           TWAIT(9, ptx::mbar_wait(&S.xfull[xsl], (qx / NX) & 1));
+          TLOG(144 + j, nf);
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
             const uint64_t xd = ptx::sdesc_sw128(ptx::smem_u32(S.Xr[xsl]), 16, 1024);
@@ -544,6 +566,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             if (j == T - 1) ptx::umma_commit(&S.p0_ok);   // D', delta and the X ring are free for the next field
           }
           __syncwarp();
+          TLOG(96 + j, nf);
         }
       }
     }
@@ -565,20 +588,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
     const uint32_t peer_recv = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.recv[half][row][0]), crank ^ 1u) : 0u;
     const uint32_t peer_recv_full = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.recv_full[ew]), crank ^ 1u) : 0u;
     const uint32_t peer_free_bar = CB > 1 ? ptx::mapa(ptx::smem_u32(&S.peer_free[ew]), crank ^ 1u) : 0u;
+    float *const bsm = &S.stg[0][0][0];   // b_f during E0 / E1 of a training step
     for (int fi = cid; fi < nfl; fi += ncl, ++nf) {
       const int f = fid(fi);
       const int fr = f / g.gc, fc = f - fr * g.gc;
       const int64_t pixbase = ((int64_t)fr * g.s * g.W + (int64_t)fc * g.s) * g.C;
+      ptx::bulk_wait_read0();   // the previous field's last dX rounds have been read out of the staging slices
       ptx::named_bar_sync(1, 32 * NEPI);
       if (etid < KP) {
         const float sg = etid < k ? P.sigma[(int64_t)f * k + etid] : 1.f;
         S.sig[etid] = sg;
         S.isig[etid] = 1.f / sg;
       }
-      for (int t = etid; t < n; t += 32 * NEPI) S.bs[t] = P.b[(int64_t)f * n + t];
+      if (!GEN)
+        for (int t = etid; t < n; t += 32 * NEPI) bsm[t] = P.b[(int64_t)f * n + t];
       ptx::named_bar_sync(1, 32 * NEPI);
       const float a = P.alpha[f];
-      const float *bf_ = S.bs;
+      // forward / encode stage the pooled output in the slices: b_f is read from global there (not the hot path)
+      const float *bf_ = GEN ? P.b + (int64_t)f * n : bsm;
+      const bool b16 = !GEN || ((((int64_t)f * n) & 3) == 0);
       double jr = 0.0, js = 0.0;
       float dap = 0.f, rsq4[4] = {0.f, 0.f, 0.f, 0.f};   // rsq4[i]: row 8i + lane/4 of this warp
       TMARK(-1);
@@ -613,32 +641,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         if (want_pooled) {   // p [m][gr][gc][ng] (forward / encode only: recv + stg are idle then)
           const int G0c = cc * NGC;   // first group of the chunk
           if constexpr (NGC >= 4) {
-            // coalesced: the warp's 32 samples x NGC groups are transposed through 4 KB of staging so that
-            // each store instruction writes whole 16-byte runs of consecutive groups of a few samples
-            constexpr int NC4 = NGC / 4;
-            float *pst = &S.recv[0][0][0] + ew * 1024;   // recv and stg are contiguous: 8 x 4 KB
+            // coalesced: the warp's 32 samples x GH groups are transposed through its 2 KB staging slice so
+            // that each store instruction writes whole 16-byte runs of consecutive groups of a few samples
+            constexpr int GH = NGC < 16 ? NGC : 16, NC4 = GH / 4;
+            float *pst = &S.stg[ew][0][0];
 #pragma unroll
-            for (int c4 = 0; c4 < NC4; ++c4)
-              *reinterpret_cast<float4 *>(pst + lane * NGC + 4 * (c4 ^ (lane % NC4))) =
-                  make_float4(pv[4 * c4], pv[4 * c4 + 1], pv[4 * c4 + 2], pv[4 * c4 + 3]);
-            __syncwarp();
+            for (int hh = 0; hh < NGC / GH; ++hh) {
 #pragma unroll
-            for (int e = lane; e < 32 * NC4; e += 32) {
-              const int r = e / NC4, c4 = e % NC4, gs = s0 + qd * 32 + r;
-              const float4 q = *reinterpret_cast<const float4 *>(pst + r * NGC + 4 * (c4 ^ (r % NC4)));
-              float *dst = P.pooled + (((int64_t)gs * g.gr + fr) * g.gc + fc) * ng + G0c + 4 * c4;
-              if (gs < m) {
-                if ((ng & 3) == 0) {   // 16-byte aligned rows
-                  if (G0c + 4 * c4 < ng) *reinterpret_cast<float4 *>(dst) = q;
-                } else {
-                  const float qq[4] = {q.x, q.y, q.z, q.w};
+              for (int c4 = 0; c4 < NC4; ++c4)
+                *reinterpret_cast<float4 *>(pst + lane * GH + 4 * (c4 ^ (lane % NC4))) =
+                    make_float4(pv[hh * GH + 4 * c4], pv[hh * GH + 4 * c4 + 1], pv[hh * GH + 4 * c4 + 2],
+                                pv[hh * GH + 4 * c4 + 3]);
+              __syncwarp();
 #pragma unroll
-                  for (int e2 = 0; e2 < 4; ++e2)
-                    if (G0c + 4 * c4 + e2 < ng) dst[e2] = qq[e2];
+              for (int e = lane; e < 32 * NC4; e += 32) {
+                const int r = e / NC4, c4 = e % NC4, gs = s0 + qd * 32 + r;
+                const float4 q = *reinterpret_cast<const float4 *>(pst + r * GH + 4 * (c4 ^ (r % NC4)));
+                const int g0 = G0c + hh * GH + 4 * c4;
+                float *dst = P.pooled + (((int64_t)gs * g.gr + fr) * g.gc + fc) * ng + g0;
+                if (gs < m) {
+                  if ((ng & 3) == 0) {   // 16-byte aligned rows
+                    if (g0 < ng) *reinterpret_cast<float4 *>(dst) = q;
+                  } else {
+                    const float qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; ++e2)
+                      if (g0 + e2 < ng) dst[e2] = qq[e2];
+                  }
                 }
               }
+              __syncwarp();
             }
-            __syncwarp();
           } else {
 #pragma unroll
             for (int q = 0; q < NGC; ++q)
@@ -671,6 +704,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         else {
           const long long tw0 = TR ? clock64() : 0;
           TWAIT(12, ptx::mbar_wait(&S.r_full[rb], (ur / NRB) & 1));
+          if (ew == 0) TLOG(32 + j, nf);
           if (TR && P.trace && lane == 0) atomicAdd(&S.tr[56 + ew], (unsigned long long)(clock64() - tw0));
         }
         ptx::tc_fence_after();
@@ -681,7 +715,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&S.r_empty[rb]);
-        jr += (double)residual32(rv, j * NT + hc, n, bf_, svalid);
+        jr += (double)residual32(rv, j * NT + hc, n, bf_, svalid, b16);
         if (step) {
           const uint32_t db_ = ud & 1;
           TWAIT(14, ptx::mbar_wait(&S.dl_empty[db_], ((ud >> 1) & 1) ^ 1));
@@ -691,6 +725,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&S.dl_full[db_]);
+          if (ew == 0) TLOG(48 + j, nf);
           ++ud;
           // db partial: column sums over this warp's 32 samples (butterfly transpose-reduce: lane l <- column l;
           // measured faster than a transpose through the staging slice, whose loads wait behind the stores)
@@ -785,13 +820,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           {
             const long long tw0 = TR ? clock64() : 0;
             TWAIT(18, ptx::mbar_wait(&S.p2_full[pb], (u2 / NB2) & 1));
+            if (ew == 0) TLOG(112 + j, nf);
             if (TR && P.trace && lane == 0) atomicAdd(&S.tr[48 + ew], (unsigned long long)(clock64() - tw0));
           }
           ptx::tc_fence_after();
           TMARK(35);
           const int swr = (lane >> 1) & 3;                     // swizzle of this lane's row (row = lane)
           float *stg = &S.stg[ew][0][0];                       // [32 rows][16] fp32, 16-byte chunks swizzled
-          const float *rcv = &S.recv[half][qd * 32][0];        // same layout, written by the peer
+          const uint32_t *rcv = &S.recv[half][qd * 32][0];     // [32 rows][16 bf16], written by the peer
           // dx = alpha W^T D - delta (both halves accumulated in TMEM) is overlap-added into the image gradient by the
           // TMA unit: each 16-column round is staged in this warp's slice as [16 patch rows][32 samples] (one
           // conflict-free 128-byte row per column) and reduce-added (cp.reduce.async.bulk.tensor .add.f32) in boxes
@@ -850,13 +886,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               ptx::tmem_ld16(tl + base + 64 + hc + 16 * crank, dw);
               ptx::tmem_ld16(tl + base + 64 + hc + 16 * (1 - crank), dw + 16);
               ptx::tmem_ld_wait();
-              // arm this warp's receive phase: 32 rows x 16 floats arrive from the peer's warp ew via st.async
-              if (lane == 0) ptx::mbar_arrive_expect_tx(&S.recv_full[ew], 32 * 16 * 4);
+              // arm this warp's receive phase: 32 rows x 16 bf16 arrive from the peer's warp ew via st.async
+              if (lane == 0) ptx::mbar_arrive_expect_tx(&S.recv_full[ew], 32 * 16 * 2);
               TWAIT(22, ptx::mbar_wait(&S.peer_free[ew], (u2 & 1) ^ 1));
+              // the peer's half crosses DSMEM in bf16 (RN-even; R25): 32 bytes per row
 #pragma unroll
-              for (int t = 0; t < 4; ++t)
-                ptx::st_async_v4(peer_recv + 16 * (t ^ swr),
-                                 make_float4(dw[16 + 4 * t], dw[17 + 4 * t], dw[18 + 4 * t], dw[19 + 4 * t]),
+              for (int t = 0; t < 2; ++t)
+                ptx::st_async_u4(peer_recv + 16 * t,
+                                 make_uint4(ptx::pack_bf16x2(dw[16 + 8 * t], dw[17 + 8 * t]),
+                                            ptx::pack_bf16x2(dw[18 + 8 * t], dw[19 + 8 * t]),
+                                            ptx::pack_bf16x2(dw[20 + 8 * t], dw[21 + 8 * t]),
+                                            ptx::pack_bf16x2(dw[22 + 8 * t], dw[23 + 8 * t])),
                                  peer_recv_full);
 #pragma unroll
               for (int t = 0; t < 4; ++t)
@@ -870,6 +910,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&S.p2_empty[pb]);   // TMEM buffer pb fully read by this warp
+            if (ew == 0) TLOG(128 + j, nf);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const int r = 8 * i + rr, o = r * 16 + 4 * (cq ^ ((r >> 1) & 3));
@@ -882,9 +923,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             TWAIT(22, ptx::mbar_wait(&S.recv_full[ew], u2 & 1));
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const int r = 8 * i + rr, o = r * 16 + 4 * (cq ^ ((r >> 1) & 3));
-              const float4 r4 = *reinterpret_cast<const float4 *>(rcv + o);
-              dq[i].x += r4.x; dq[i].y += r4.y; dq[i].z += r4.z; dq[i].w += r4.w;
+              const int r = 8 * i + rr;
+              const uint2 v = *reinterpret_cast<const uint2 *>(rcv + r * 8 + 2 * cq);   // 4 bf16 of columns 4cq..
+              dq[i].x += __uint_as_float(v.x << 16);
+              dq[i].y += __uint_as_float(v.x & 0xFFFF0000u);
+              dq[i].z += __uint_as_float(v.y << 16);
+              dq[i].w += __uint_as_float(v.y & 0xFFFF0000u);
             }
             __syncwarp();
             if (lane == 0)   // receive slice read: the peer may send the next tile (reads only; relaxed suffices)
@@ -1010,6 +1054,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
   if (P.trace && threadIdx.x < 64) atomicAdd(&P.trace[threadIdx.x], S.tr[threadIdx.x]);
 #undef TWAIT
 #undef TMARK
+#undef TLOG
   if (CB > 1) ptx::cluster_sync();
   if (warp == 1) ptx::tmem_dealloc<512>(tb);
 }

@@ -49,7 +49,7 @@ for _ in range(steps):
     run()
 torch.cuda.synchronize()
 ms, nl = L.profile_read()
-out = (C.c_ulonglong * 64)()
+out = (C.c_ulonglong * (64 + 256))()
 lcae.check(lib.lcae_dev_trace(L.h, 0, out))
 ctas = min(shape.fields * ((shape.batch + 127) // 128), 148 // ((shape.batch + 127) // 128) * ((shape.batch + 127) // 128))
 per = lambda v: v / ctas / steps  # noqa: E731
@@ -61,3 +61,18 @@ for i in sorted(NAMES):
 print("  per epilogue warp (warp = 2 + w, TMEM quarter w % 4, column half w // 4): wait p2_full / wait r_full")
 for w in range(8):
     print(f"    w{w} (warp {w + 2}, SMSP {(w + 2) % 4}): {100 * per(out[48 + w]) / tot:5.1f}%  {100 * per(out[56 + w]) / tot:5.1f}%")
+
+# timeline of CTA 0's third field (traced variant): event times in us relative to the first R issue
+tl = list(out[64:64 + 256])
+if any(tl):
+    clk = 1.965e3   # cycles per us at the maximum SM clock (approximate)
+    t0 = min(v for v in tl[0:16] if v)
+    f = lambda v: (v - t0) / clk if v else float("nan")  # noqa: E731
+    print("pass 1 (us): j  W_ready  X_ready  R_issued  G_issued  R_seen(w2)  delta_done(w2)")
+    for j in range(16):
+        print(f"  {j:2d} {f(tl[80 + j]):8.2f} {f(tl[64 + j]):8.2f} {f(tl[j]):8.2f} {f(tl[16 + j]):8.2f} {f(tl[32 + j]):8.2f} "
+              f"{f(tl[48 + j]):8.2f}")
+    print("pass 2 (us): j  W_ready  d_reloaded  buf_free  X_ready  issued  seen(w2)  freed(w2)")
+    for j in range(16):
+        print(f"  {j:2d} {f(tl[176 + j]):8.2f} {f(tl[160 + j]):8.2f} {f(tl[192 + j]):8.2f} {f(tl[144 + j]):8.2f} "
+              f"{f(tl[96 + j]):8.2f} {f(tl[112 + j]):8.2f} {f(tl[128 + j]):8.2f}")
