@@ -83,6 +83,17 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Polling wait (test_wait never suspends the warp): for the MMA issuer, whose every step waits on a barrier
+// that is usually already complete or about to complete.
+__device__ __forceinline__ void mbar_wait_poll(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAITP_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAITP_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 // cp.async (LDGSTS) completion tracked by an mbarrier: arrive when all prior cp.async of this thread land.
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t *bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");

@@ -210,6 +210,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
   // trace: lane 0 of the producers / MMA warp and of epilogue warp 2 record their barrier-wait cycles
   const bool trec = TR && P.trace != nullptr && lane == 0 && (warp <= 2 || warp == XWARP);
   const long long t_start = clock64();
+// the MMA issuer polls (LCAE_MMA_WAIT_POLL) or suspends (default) on its barriers
+#ifdef LCAE_MMA_WAIT_POLL
+#define MMA_WAIT(...) ptx::mbar_wait_poll(__VA_ARGS__)
+#else
+#define MMA_WAIT(...) ptx::mbar_wait(__VA_ARGS__)
+#endif
 #define TWAIT(IDX, ...)                                                                          \
   do {                                                                                           \
     if (trec) {                                                                                  \
@@ -433,7 +439,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       uint32_t qw = 0, q0 = 0, q1 = 0, qx = 0, nf = 0, ur = 0, ud = 0, u2 = 0, qd2 = 0;
       auto wst = [&](uint32_t qq) { return ptx::smem_u32(S.Wr[qq % NW]); };
       auto wait_w = [&](uint32_t qq) {
-        TWAIT(0, ptx::mbar_wait(&S.wfull[qq % NW], (qq / NW) & 1));
+        TWAIT(0, MMA_WAIT(&S.wfull[qq % NW], (qq / NW) & 1));
         ptx::tc_fence_after();
       };
       // D = A^T W~_j: A = H' or D' (K-major [128][128]), W~_j MN-major (elected lane only)
@@ -455,14 +461,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         // overlap this field's pooling epilogue)
         const uint32_t ucol = enc ? 128 * (nf & 3) : 384;
         if (enc) {
-          TWAIT(2, ptx::mbar_wait(&S.ue[nf & 3], ((nf >> 2) & 1) ^ 1));
+          TWAIT(2, MMA_WAIT(&S.ue[nf & 3], ((nf >> 2) & 1) ^ 1));
           ptx::tc_fence_after();
         }
         for (int j = 0; j < T; ++j, ++qw, ++q0) {
           wait_w(qw);
-          TWAIT(1, ptx::mbar_wait(&S.p0full[q0 % NP0], (q0 / NP0) & 1));
-          ptx::tc_fence_after();
-          ptx::fence_proxy_async_smem();
+          TWAIT(1, MMA_WAIT(&S.p0full[q0 % NP0], (q0 / NP0) & 1));
+          ptx::tc_fence_after();   // (TMA-written operands: no proxy fence needed on this side)
           if (ptx::elect_one()) {
             const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(p0slot(S, q0 % NP0)), 8192, 1024);
             const uint64_t bd = ptx::sdesc_sw128(wst(qw), 16, 1024);
@@ -477,15 +482,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         }
         if (enc) continue;
         // ---- pass 1: R_j - X_j, then G += delta_{j-GLAG} W~_{j-GLAG}^T
-        TWAIT(3, ptx::mbar_wait(&S.h_ready, nf & 1));
-        ptx::tc_fence_after();
-        ptx::fence_proxy_async_smem();
+        TWAIT(3, MMA_WAIT(&S.h_ready, nf & 1));
+        ptx::tc_fence_after();   // H' was fenced to the async proxy by its writers before their arrivals
         const uint32_t qw1 = qw;
         auto issue_G = [&](int j) {
           const uint32_t qj = qw1 + j, db_ = ud & 1;
-          TWAIT(5, ptx::mbar_wait(&S.dl_full[db_], (ud >> 1) & 1));
-          ptx::tc_fence_after();
-          ptx::fence_proxy_async_smem();
+          TWAIT(5, MMA_WAIT(&S.dl_full[db_], (ud >> 1) & 1));
+          ptx::tc_fence_after();   // delta_j: fenced by its writers
           if (ptx::elect_one()) {
             const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(S.Dl[db_]), 16, 1024);
             const uint64_t bd = ptx::sdesc_sw128(wst(qj), 16, 1024);
@@ -504,11 +507,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           wait_w(qw);
           TLOG(80 + j, nf);
           const uint32_t rb = ur % NRB, s1 = q1 % np1;
-          TWAIT(4, ptx::mbar_wait(&S.r_empty[rb], ((ur / NRB) & 1) ^ 1));
-          TWAIT(44, ptx::mbar_wait(&S.p1full[s1], (q1 / np1) & 1));
+          TWAIT(4, MMA_WAIT(&S.r_empty[rb], ((ur / NRB) & 1) ^ 1));
+          TWAIT(44, MMA_WAIT(&S.p1full[s1], (q1 / np1) & 1));
           TLOG(64 + j, nf);
           ptx::tc_fence_after();
-          ptx::fence_proxy_async_smem();
           if (ptx::elect_one()) {
             mma_aw(64 * rb, dH_k, wst(qw));
             mma_negx(64 * rb, ptx::smem_u32(p1slot(S, s1)));
@@ -525,17 +527,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         // ---- pass 2 (TMEM: NB2 buffers [dX | dW] in [0,384)): delta_j is the pass-1 tile reloaded from global
         //   dx^T_j = D'^T W~_j + delta_j^T (-I)   (alpha folded into D')
         //   dW_j   = H' delta_j^T + D' X_j^T
-        TWAIT(6, ptx::mbar_wait(&S.d_ready, nf & 1));
-        ptx::tc_fence_after();
-        ptx::fence_proxy_async_smem();
+        TWAIT(6, MMA_WAIT(&S.d_ready, nf & 1));
+        ptx::tc_fence_after();   // D': fenced by its writers
         for (int j = 0; j < T; ++j, ++qw, ++u2, ++qx, ++qd2) {
           const uint32_t pb = u2 % NB2, xsl = qx % NX, sd = qd2 & 1;
           const uint32_t dcol = 128 * pb;
           wait_w(qw);
           TLOG(176 + j, nf);
-          TWAIT(8, ptx::mbar_wait(&S.d2full[sd], (qd2 >> 1) & 1));
+          TWAIT(8, MMA_WAIT(&S.d2full[sd], (qd2 >> 1) & 1));
           TLOG(160 + j, nf);
-          TWAIT(7, ptx::mbar_wait(&S.p2_empty[pb], ((u2 / NB2) & 1) ^ 1));
+          TWAIT(7, MMA_WAIT(&S.p2_empty[pb], ((u2 / NB2) & 1) ^ 1));
           TLOG(192 + j, nf);
           ptx::tc_fence_after();
           const uint32_t dl = ptx::smem_u32(S.Dl[sd]);
@@ -552,7 +553,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
               ptx::umma_bf16(tb + dcol + 64, adv(dH_mn, kk * 2048), adv(dlmn, kk * 2048), id_dw1, kk > 0);
           }
           __syncwarp();
-          TWAIT(9, ptx::mbar_wait(&S.xfull[xsl], (qx / NX) & 1));
+          TWAIT(9, MMA_WAIT(&S.xfull[xsl], (qx / NX) & 1));
           TLOG(144 + j, nf);
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
@@ -726,6 +727,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&S.dl_full[db_]);
           if (ew == 0) TLOG(48 + j, nf);
+          if (j >= 4 && j < 10) TLOG(208 + (j - 4) * 8 + ew, nf);   // every warp's delta_j, tiles 4..9
           ++ud;
           // db partial: column sums over this warp's 32 samples (butterfly transpose-reduce: lane l <- column l;
           // measured faster than a transpose through the staging slice, whose loads wait behind the stores)
@@ -1055,6 +1057,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
 #undef TWAIT
 #undef TMARK
 #undef TLOG
+#undef MMA_WAIT
   if (CB > 1) ptx::cluster_sync();
   if (warp == 1) ptx::tmem_dealloc<512>(tb);
 }

@@ -76,3 +76,6 @@ if any(tl):
     for j in range(16):
         print(f"  {j:2d} {f(tl[176 + j]):8.2f} {f(tl[160 + j]):8.2f} {f(tl[192 + j]):8.2f} {f(tl[144 + j]):8.2f} "
               f"{f(tl[96 + j]):8.2f} {f(tl[112 + j]):8.2f} {f(tl[128 + j]):8.2f}")
+    print("pass 1 delta_j done per epilogue warp (us; warp = 2 + w):")
+    for jj in range(6):
+        print(f"  j={4 + jj}: " + " ".join(f"{f(tl[208 + jj * 8 + w]):7.2f}" for w in range(8)))
