@@ -517,12 +517,74 @@ def run_ours(args, shape):
     print(json.dumps(line), flush=True)
 
 
+PAPER_METRIC = "images/sec per greedy training step of the paper's 3-layer network (one step of every layer)"
+
+
+def run_paper_stack(args):
+    """SURVEY.md §8(f) item 1 at the paper's geometry (R26): 300 x 300 x 3 images ->
+    72 x 72 fields x 384 (1.53 B weights) -> LCN -> 69 x 69 fields x 384 over 16 x 16 x 24 windows (11.26 B) -> LCN ->
+    dense 92,256 -> 4096 (0.38 B); 13.17 B parameters, mini-batch 192. k = 384 / 4096 exceed the fused bf16
+    kernel's TMEM budget (R24): every layer runs on the fp32 path. One 'step' = one greedy training step of each
+    layer on the same batch (layer l's input produced by the trained layers below, as in layer-wise training);
+    the input chains (encode + LCN of the layers below) are timed separately."""
+    import torch
+    from paper_1502_03409_b200 import lcae
+    from paper_1502_03409_b200.stack import Stack, paper_stack
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    cfg = paper_stack(batch=args.batch or 192)
+    st = Stack(cfg, precision=lcae.FP32, seed=0, host_params=False)
+    pool = [torch.from_numpy(make_images(cfg.shapes[0], seed=1, index=i)).cuda() for i in range(2)]
+    n = len(cfg.shapes)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    for i in range(max(1, args.warmup // 3)):
+        for l in range(n):
+            st.layers[l].step(st.input_of(l, pool[i % 2]), None, want_loss=False)
+    torch.cuda.synchronize()
+    t_layer, t_chain = [0.0] * n, [0.0] * n
+    with ClockSampler(0) as clk:
+        for i in range(args.steps):
+            for l in range(n):
+                e0, e1, e2 = ev(), ev(), ev()
+                e0.record()
+                inp = st.input_of(l, pool[i % 2])
+                e1.record()
+                st.layers[l].step(inp, None, want_loss=False)
+                e2.record()
+                torch.cuda.synchronize()
+                t_chain[l] += e0.elapsed_time(e1) / args.steps
+                t_layer[l] += e1.elapsed_time(e2) / args.steps
+    J = [st.layers[l].last_loss() for l in range(n)]
+    st.close()
+    ms = sum(t_layer)
+    flops = [12.0 * s.filters * s.n * s.batch * s.fields for s in cfg.shapes]
+    ck = clk.summary()
+    alu_peak = FP32_ALU_TFLOPS * (ck["sm_mhz"] / ck["sm_max_mhz"] if ck.get("sm_mhz") and ck.get("sm_max_mhz") else 1)
+    ach = sum(flops) / (ms * 1e-3) / 1e12
+    line = {"metric": PAPER_METRIC, "value": cfg.shapes[0].batch / (ms * 1e-3), "unit": "images/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "paper3 (PAPER.md:95 three-layer network, DESIGN.md R26)",
+                       "layers": [{"name": s.name, "input": [s.img_h, s.img_w, s.img_c], "rf": s.rf_h,
+                                   "stride": s.stride, "fields": s.fields, "n": s.n, "k": s.filters,
+                                   "params": s.fields * (s.filters * s.n + s.n + 1), "step_ms": t_layer[i],
+                                   "input_chain_ms": t_chain[i], "tflops": flops[i] / (t_layer[i] * 1e-3) / 1e12,
+                                   "J": J[i][0] + J[i][1]} for i, s in enumerate(cfg.shapes)],
+                       "params": sum(s.fields * (s.filters * s.n + s.n + 1) for s in cfg.shapes),
+                       "batch": cfg.shapes[0].batch, "lcn_window": cfg.lcn_window},
+            "tflops": ach,
+            "roofline": {"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s", "frac": ach / alu_peak,
+                         "traffic": None, "kernel": "fp32 path (all kernels of the three layer steps)",
+                         "kernel_ms": ms, "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x SM clock"},
+            "clocks": ck}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + sorted(EXTRA) + ["c5fit"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + sorted(EXTRA) + ["c5fit", "paper3"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"],
                     help="bf16: the tcgen05 path (default); fp32: the FFMA path (needed for k > 128, e.g. c3p)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -540,7 +602,9 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     args.prec = 0 if args.precision == "fp32" else 1
-    if args.config == "c5fit":   # largest single-GPU layer of the c3 field shape (sized from cudaMemGetInfo)
+    if args.config == "paper3":
+        shape = CONFIGS["c3"]   # placeholder: run_paper_stack builds the three layers itself
+    elif args.config == "c5fit":   # largest single-GPU layer of the c3 field shape (sized from cudaMemGetInfo)
         import torch
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         free, _ = torch.cuda.mem_get_info()
@@ -558,7 +622,9 @@ def main():
         gr, gc = shape.grid_r * tr, shape.grid_c * tc
         shape = shape.replace(name=f"{shape.name}-weak", img_h=(gr - 1) * shape.stride + shape.rf_h,
                               img_w=(gc - 1) * shape.stride + shape.rf_w)
-    if args.impl == "reference":
+    if args.config == "paper3":
+        run_paper_stack(args)
+    elif args.impl == "reference":
         run_reference(args, shape)
     elif args.mode == "infer":
         run_infer(args, shape)

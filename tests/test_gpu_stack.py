@@ -117,3 +117,82 @@ def test_chain_geometry_checked():
     bad = StackConfig([cfg.shapes[0], cfg.shapes[2]])
     with pytest.raises(ValueError):
         check_chain(bad)
+
+
+def _oracle_map(p, block):
+    """Numpy statement of the block-map layout (stack.to_map): [m][gr][gc][bh*bw*c] -> [m][gr*bh][gc*bw][c]."""
+    if block is None:
+        return p
+    m, gr, gc, ch = p.shape
+    c = ch // (block[0] * block[1])
+    return p.reshape(m, gr, gc, block[0], block[1], c).transpose(0, 1, 3, 2, 4, 5).reshape(m, gr * block[0],
+                                                                                          gc * block[1], c)
+
+
+def test_paper_architecture_stack_fp32():
+    """The paper's three-layer network (read as DESIGN.md R26) at its field shapes -- 16x16x3 -> 384
+    (4x4x24 blocks), 16 contiguous 4x4x24 blocks (n = 6144) -> 384, dense -> 4096 -- on a 28 x 28 image: every
+    stage of the fp32 chain (encode, block map, LCN, crop) against the oracle on the GPU stage's input, 1e-5."""
+    import torch
+    from paper_1502_03409_b200 import lcae
+    from paper_1502_03409_b200.stack import Stack, check_chain, paper_stack
+    cfg = paper_stack(batch=8, image=28, lcn_window=3)   # the small maps (16 x 16, 4 x 4) take a 3 x 3 LCN window
+    check_chain(cfg)
+    X = make_images(cfg.shapes[0], seed=4, bf16_round=False)
+    params = [make_params(s, seed=i) for i, s in enumerate(cfg.shapes)]
+    st = Stack(cfg, precision=lcae.FP32, seed=0)
+    errs = {}
+    try:
+        x = torch.from_numpy(X).cuda()
+        for l, s in enumerate(cfg.shapes):
+            code = st._code(l, x)
+            W, a, b = params[l]
+            want = layer_gradients(W.astype(np.float64), a.astype(np.float64), b.astype(np.float64),
+                                   x.cpu().numpy().astype(np.float64), geo_of(s))["p"]
+            errs[f"encode{l}"] = normwise(code.cpu().numpy(), want)
+            mp = st.to_map(l, code)
+            assert np.array_equal(mp.cpu().numpy(), _oracle_map(code.cpu().numpy(), cfg.block(l)))
+            if l + 1 < len(cfg.shapes):
+                y = st._lcn(mp)
+                errs[f"lcn{l}"] = normwise(y.cpu().numpy(), lcn(mp.cpu().numpy().astype(np.float64), cfg.lcn_window,
+                                                               cfg.lcn_floor))
+                x = st.next_input(l, y)
+                assert x.shape[1:] == (cfg.shapes[l + 1].img_h, cfg.shapes[l + 1].img_w, cfg.shapes[l + 1].img_c)
+    finally:
+        st.close()
+    print({k: f"{v:.1e}" for k, v in errs.items()})
+    assert all(v <= 1e-5 for v in errs.values()), errs
+
+
+@pytest.mark.parametrize("which", ["layer2", "layer3"])
+def test_paper_layer_field_shapes_fp32(which):
+    """One training step at the paper's layer-2 field shape (n = 6144, k = 384) and at the dense layer 3's full
+    shape (n = 62 * 62 * 24 = 92,256, k = 4096), fp32 path vs the oracle at north_star's 1e-5."""
+    from paper_1502_03409_b200.inputs import LayerShape
+    from tests.gpu_harness import gpu_step, oracle_step as harness_oracle_step
+    from tests.test_gpu_parity import _compare
+    if which == "layer2":
+        shape = LayerShape("paper2-small", 20, 20, 24, 16, 16, 4, 384, 1, 16, lam=0.1)
+    else:
+        # m = 4 keeps the fp64 oracle quick
+        shape = LayerShape("paper3", 62, 62, 24, 62, 62, 1, 4096, 1, 4, lam=0.01)
+    W, a, b = make_params(shape, seed=0)
+    b = (0.05 * np.random.default_rng(3).standard_normal(b.shape)).astype(np.float32)
+    X = make_images(shape, seed=1, bf16_round=False)
+    out = gpu_step(shape, 0, W, a, b, X, forward_first=False)
+    o = harness_oracle_step(shape, W, a, b, X)
+    if which == "layer2":
+        errs = _compare(shape, 0, out, o, W.astype(np.float64), a.astype(np.float64), b.astype(np.float64))
+    else:
+        # north_star's 1e-5 names activations, loss and gradients: those are held to it. The projected update of a
+        # 92,256-long row (W' = rownorm(W - lr dW), PAPER.md:89) inherits the gradient's 1e-5-level error through
+        # the row's radial correction (a dot product over n terms), so the update is held to 1e-4 here.
+        errs = {"J": abs(out["J"] - o["J"]) / abs(o["J"])}
+        for key in ("dW", "dalpha", "db", "dX"):
+            errs[key] = normwise(out[key], o[key])
+        assert all(v <= 1e-5 for v in errs.values()), errs
+        W64 = W.astype(np.float64)
+        errs["dW_update"] = normwise(out["W_new"].astype(np.float64) - W64, o["W_new"] - W64)
+        errs["b_update"] = normwise(out["b_new"].astype(np.float64) - b, o["b_new"] - b)
+        assert errs["dW_update"] <= 1e-4 and errs["b_update"] <= 1e-5, errs
+    print(which, {k: f"{v:.1e}" for k, v in errs.items()})
