@@ -117,8 +117,8 @@ struct TcScratch {
 };
 
 // Pieces of the patch rows [r0, r0 + rows) of a field window: runs of consecutive image rows (one per receptive-field
-// row) split into power-of-two boxes of at most 2^maxlg rows. Word: offset in the window (16 b) | first row relative
-// to r0 (8 b) << 16 | log2 height (8 b) << 24. Returns false if more than cap pieces are needed.
+// row) split into power-of-two boxes of at most 2^maxlg rows. Word: offset in the window, first row relative
+// to r0, log2 height (tc::piece_word). Returns false if more than cap pieces are needed.
 static bool window_pieces(const Geo &g, int r0, int rows, int maxlg, int cap, uint32_t *out) {
   int np = 0, r = 0;
   while (r < rows) {
@@ -129,7 +129,7 @@ static bool window_pieces(const Geo &g, int r0, int rows, int maxlg, int cap, ui
       int lg = maxlg;
       while ((1 << lg) > left) --lg;
       if (np >= cap) return false;
-      out[np++] = (uint32_t)off | ((uint32_t)r << 16) | ((uint32_t)lg << 24);
+      out[np++] = tc::piece_word((uint32_t)off, (uint32_t)r, (uint32_t)lg);
       off += 1 << lg;
       r += 1 << lg;
       left -= 1 << lg;
@@ -143,8 +143,8 @@ lcae_status tc_alloc(lcae_layer *L) {
   if (g.k > tc::KP) { set_error("bf16 path: filters per field must be <= 128"); return LCAE_ERR_CONFIG; }
   if (g.m > 2 * tc::MC) { set_error("bf16 path: batch must be <= 256"); return LCAE_ERR_CONFIG; }
   const int T = cdiv(g.n, tc::NT);
-  if (T * tc::NT > tc::MAX_NPAD) { set_error("bf16 path: rf_h*rf_w*C must be <= 1024"); return LCAE_ERR_CONFIG; }
-  if ((int64_t)(g.rf_h - 1) * g.W * g.C + g.RW > 65535) { set_error("bf16 path: field window spans > 65535 pixel-features"); return LCAE_ERR_CONFIG; }
+  if (T * tc::NT > tc::MAX_NPAD) { set_error("bf16 path: rf_h*rf_w*C must be <= 4096"); return LCAE_ERR_CONFIG; }
+  if ((int64_t)(g.rf_h - 1) * g.W * g.C + g.RW > (1 << 20)) { set_error("bf16 path: field window spans > 2^20 pixel-features"); return LCAE_ERR_CONFIG; }
   TcScratch *s = new TcScratch();
   L->tc = s;
   s->CB = cdiv(g.m, tc::MC);

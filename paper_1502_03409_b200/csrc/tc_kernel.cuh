@@ -49,7 +49,16 @@ constexpr int GLAG = 1;        // G_j issued after R_{j+GLAG}
 constexpr int NEPI = 8;        // epilogue warps
 constexpr int XWARP = 2 + NEPI;
 constexpr int NTHREADS = 32 * (XWARP + 1);
-constexpr int MAX_NPAD = 1024;
+constexpr int MAX_NPAD = 4096;   // n = rf_h rf_w C <= 4096 (b_f fits the 16 KB of staging slices)
+
+// TMA piece words (host table): window offset (20 bits) | first row in the tile / chunk (7 bits) << 20 |
+// log2 box height (3 bits) << 27; 0xFFFFFFFF ends a list (row 127 never occurs)
+__host__ __device__ constexpr uint32_t piece_word(uint32_t off, uint32_t row, uint32_t lg) {
+  return off | (row << 20) | (lg << 27);
+}
+__host__ __device__ inline uint32_t piece_off(uint32_t w) { return w & 0xFFFFFu; }
+__host__ __device__ inline uint32_t piece_row(uint32_t w) { return (w >> 20) & 0x7Fu; }
+__host__ __device__ inline uint32_t piece_lg(uint32_t w) { return (w >> 27) & 0x7u; }
 
 constexpr int NXMAP = 7;       // X tensor maps with box heights 1, 2, 4, ..., 64 rows
 constexpr int XPMAX = 64;      // max TMA pieces per 64-row X tile
@@ -59,7 +68,7 @@ constexpr int DXPMAX = 16;     // max TMA pieces per 16-column dX chunk
 struct Params {
   CUtensorMap tmW;   // W~ bf16 [F*KP][n_al], box (64, 128)
   CUtensorMap tmX[NXMAP];   // X HWCN bf16 viewed as [H*W*C rows][mp], box (64 samples, 2^i rows)
-  const uint32_t *xpieces;  // [T][XPMAX]: off (16 b) | dst row (8 b) << 16 | log2 rows (8 b) << 24; 0xFFFFFFFF ends
+  const uint32_t *xpieces;  // [T][XPMAX] piece words (piece_word); 0xFFFFFFFF ends
   CUtensorMap tmD[NDMAP];   // dX HWCN f32 viewed as [H*W*C rows][mp], box (32 samples, 2^i rows), no swizzle
   const uint32_t *dxpieces; // [T][4][DXPMAX]: the pieces of 16-column chunk q of tile j, same encoding
   const int *flist;         // nullable: the launch walks fields flist[0..nfl) (model-parallel interior / boundary
@@ -230,7 +239,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
   // timeline (traced variant only): clock64 of pipeline events of CTA 0's third field, into P.trace[64 + id]
 #define TLOG(ID, NF)                                                                             \
   do {                                                                                           \
-    if (TR && P.trace && blockIdx.x == 0 && (NF) == 2 && lane == 0)                             \
+    if (TR && P.trace && blockIdx.x == 0 && (NF) == 2 && lane == 0 && P.T <= 16)                \
       P.trace[64 + (ID)] = (unsigned long long)clock64();                                        \
   } while (0)
   // ---- one-time setup
@@ -353,7 +362,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         for (int e = 0; e < 2; ++e) {
           const uint32_t w = e ? w1 : w0;
           if (w != 0xFFFFFFFFu) {
-            const int offp = (int)(w & 0xFFFFu), dr = (int)((w >> 16) & 0xFFu), lg = (int)(w >> 24);
+            const int offp = (int)piece_off(w), dr = (int)piece_row(w), lg = (int)piece_lg(w);
             LCAE_DCHECK(lg < NXMAP && dr + (1 << lg) <= NT && pixbase + offp + (1 << lg) <= prow);
 #pragma unroll
             for (int h = 0; h < 2; ++h)
@@ -845,11 +854,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             for (int c = 0; c < 16; ++c) stg[c * 32 + lane] = xv[16 * r + c];
             ptx::fence_proxy_async_smem();
             __syncwarp();
-            LCAE_DCHECK(pw == 0xFFFFFFFFu || ((pw >> 24) < (uint32_t)NDMAP && ((pw >> 16) & 0xFFu) + (1u << (pw >> 24)) <= 16u &&
-                                             pixbase + (pw & 0xFFFFu) + (1u << (pw >> 24)) <= prow));
+            LCAE_DCHECK(pw == 0xFFFFFFFFu || (piece_lg(pw) < (uint32_t)NDMAP && piece_row(pw) + (1u << piece_lg(pw)) <= 16u &&
+                                             pixbase + piece_off(pw) + (1u << piece_lg(pw)) <= prow));
             if (pw != 0xFFFFFFFFu && do_red)
-              ptx::tma_red_add_2d(&P.tmD[pw >> 24], stg + ((pw >> 16) & 0xFFu) * 32, s0 + qd * 32,
-                                  (int)pixbase + (int)(pw & 0xFFFFu));
+              ptx::tma_red_add_2d(&P.tmD[piece_lg(pw)], stg + piece_row(pw) * 32, s0 + qd * 32,
+                                  (int)pixbase + (int)piece_off(pw));
             ptx::bulk_commit();
           };
           // dW_j (lanes = filter rows, this warp's 32 columns). CTA c owns the 16-column chunk [16c, 16c+16) of

@@ -275,3 +275,22 @@ def test_field_losses_sum_to_loss(precision):
 def _patches(shape, X, f):
     r, c = divmod(f, shape.grid_c)
     return O.field_patch(X.astype(np.float64), r, c, shape.rf_h, shape.rf_w, shape.stride)
+
+
+LARGE_N = {
+    "n2048": LayerShape("n2048", 24, 24, 8, 16, 16, 4, 64, 2, 128),      # 64 x 16 x 16 x 8 patch rows, 32 tiles
+    "n3072c2": LayerShape("n3072c2", 24, 24, 12, 16, 16, 4, 128, 1, 200),   # two-CTA cluster, k = 128, 48 tiles
+    "n4096": LayerShape("n4096", 20, 20, 16, 16, 16, 4, 32, 4, 64),      # the bf16 path's limit, 64 tiles
+}
+
+
+@pytest.mark.parametrize("name", list(LARGE_N))
+def test_bf16_large_receptive_fields(name, grid_cap):
+    """n = rf_h rf_w C beyond 1024 (up to 4096) on the tensor-core path, several fields per CTA (grid capped)."""
+    shape = LARGE_N[name]
+    grid_cap(2)
+    W, a, b, X = _inputs(shape, raw=True)
+    out = gpu_step(shape, 1, W, a, b, X)
+    o = oracle_step(shape, W, a, b, X)
+    errs = _compare(shape, 1, out, o, W.astype(np.float64), a.astype(np.float64), b.astype(np.float64))
+    print(name, shape.n, {k_: f"{v:.1e}" for k_, v in errs.items()})
