@@ -63,15 +63,30 @@ static __device__ __noinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 #else
+#ifndef LCAE_WAIT_NOHINT
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"   // suspends (no issue-slot spin)
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"   // suspends (NANOSLEEP.SYNCS loop)
       "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(0x989680u)
       : "memory");
 }
+#else
+// try_wait without a time hint (LCAE_WAIT_NOHINT): the hardware's own bounded wait per TRYWAIT instead of the
+// NANOSLEEP.SYNCS re-check loop the hinted form compiles to (~12% of the step kernel's issued instructions are
+// those loops); A/B on c3: no difference, so the hinted form stays the default
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+#endif
 #endif
 // Spin-free wait for waiters that are themselves latency-critical consumers: same instruction, no hint.
 __device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
