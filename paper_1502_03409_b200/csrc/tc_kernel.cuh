@@ -152,20 +152,24 @@ __device__ __forceinline__ void red_v4(float *p, float a, float b, float c, floa
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d));
 }
 
-// e = (R - x) + b over this warp's 32 columns of a tile for this thread's sample; rv <- delta = 2e (masked).
-__device__ __forceinline__ float residual32(float (&rv)[32], int c0, int n, const float *bf_, bool svalid, bool b16) {
+// e = (R - x) + b over this warp's 32 columns of a tile for this thread's sample; rv <- delta = 2e (masked);
+// returns sum delta^2 = 4 sum e^2. b2 holds 2 b (the training step keeps 2 b_f in shared memory, b2_ready) or b:
+// delta = fma(2, R - x, 2b) rounds exactly as 2 ((R - x) + b) (scaling by 2 is exact), one FFMA per element.
+__device__ __forceinline__ float residual32(float (&rv)[32], int c0, int n, const float *b2, bool svalid, bool b16,
+                                            bool b2_ready) {
   float jr = 0.f;
-  const float4 *b4 = reinterpret_cast<const float4 *>(bf_ + c0);   // c0 % 32 == 0: 16-byte aligned broadcasts
+  const float4 *b4 = reinterpret_cast<const float4 *>(b2 + c0);   // c0 % 32 == 0: 16-byte aligned broadcasts
+  const float bs = b2_ready ? 1.f : 2.f;
   if (svalid && c0 + 32 <= n && b16) {   // full run (all but the ragged last tile): no masking
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const float4 bv = b4[q];
-      const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
+      const float bb[4] = {bv.x * bs, bv.y * bs, bv.z * bs, bv.w * bs};
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const float e = rv[4 * q + t] + bb[t];
-        jr = fmaf(e, e, jr);
-        rv[4 * q + t] = 2.f * e;
+        const float d = fmaf(2.f, rv[4 * q + t], bb[t]);
+        jr = fmaf(d, d, jr);
+        rv[4 * q + t] = d;
       }
     }
     return jr;
@@ -173,10 +177,10 @@ __device__ __forceinline__ float residual32(float (&rv)[32], int c0, int n, cons
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
     const int nn = c0 + c;
-    float e = rv[c] + (nn < n ? bf_[nn] : 0.f);
-    e = (svalid && nn < n) ? e : 0.f;
-    jr = fmaf(e, e, jr);
-    rv[c] = 2.f * e;
+    float d = fmaf(2.f, rv[c], nn < n ? b2[nn] * bs : 0.f);
+    d = (svalid && nn < n) ? d : 0.f;
+    jr = fmaf(d, d, jr);
+    rv[c] = d;
   }
   return jr;
 }
@@ -610,8 +614,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         S.sig[etid] = sg;
         S.isig[etid] = 1.f / sg;
       }
-      if (!GEN)
-        for (int t = etid; t < n; t += 32 * NEPI) bsm[t] = P.b[(int64_t)f * n + t];
+      if (!GEN)   // 2 b_f (see residual32)
+        for (int t = etid; t < n; t += 32 * NEPI) bsm[t] = 2.f * P.b[(int64_t)f * n + t];
       ptx::named_bar_sync(1, 32 * NEPI);
       const float a = P.alpha[f];
       // forward / encode stage the pooled output in the slices: b_f is read from global there (not the hot path)
@@ -725,7 +729,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&S.r_empty[rb]);
-        jr += (double)residual32(rv, j * NT + hc, n, bf_, svalid, b16);
+        jr += 0.25 * (double)residual32(rv, j * NT + hc, n, bf_, svalid, b16, !GEN);   // sum e^2 (x 1/4 exact)
         if (step) {
           const uint32_t db_ = ud & 1;
           TWAIT(14, ptx::mbar_wait(&S.dl_empty[db_], ((ud >> 1) & 1) ^ 1));
