@@ -1001,13 +1001,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
                 }
                 // the accumulator holds sigma_r dJ/dW: dJ/dW = acc / sigma_r; W~' = sigma_r W~ - lr dJ/dW
                 const float cr = nlr * isgr[i];
+                // plain SGD (lean): rownorm(sigma W~ - lr acc / sigma) = rownorm(W~ - (lr / sigma^2) acc) for
+                // sigma > 0, so W~ is updated without the sigma scale (one FFMA per element) and sigma' = 1 / ||W~'||
+                // follows in the finalize kernel as before; with momentum the velocity lives in W's scale
+                const float cr2 = cr * isgr[i];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                   const float acc = (fullc || cc0 + e < n) ? d0[e] : 0.f;
                   d[e] = acc;
-                  float upd = cr * acc;
-                  if (has_v) { upd = fmaf(P.mu, vo[e], upd); vo[e] = upd; }
-                  wn[e] = fmaf(sgr[i], wo4[e], upd);
+                  if constexpr (FULL) {
+                    float upd = cr * acc;
+                    if (has_v) { upd = fmaf(P.mu, vo[e], upd); vo[e] = upd; }
+                    wn[e] = fmaf(sgr[i], wo4[e], upd);
+                  } else {
+                    wn[e] = fmaf(cr2, acc, wo4[e]);
+                  }
                   rsq4[i] = fmaf(wn[e], wn[e], rsq4[i]);
                 }
                 ptx::st_f4_ef(wp_, make_float4(wn[0], wn[1], wn[2], wn[3]), pol_ef);
