@@ -89,10 +89,91 @@ __global__ void __launch_bounds__(256) sgemm_batched(int M, int N, int K, OpA A,
   }
 }
 
+// The same contract on 128 x 128 tiles, 8 x 8 accumulators per thread (two 4 x 4 quadrants 64 rows / columns
+// apart, read with 16-byte shared loads), K in steps of 8 with the next step's operands loaded into registers
+// while the current one computes. Used when M, N >= 128 (the paper-exact layers, k = 384 / 4096).
+constexpr int BM = 128, BN = 128, BK = 8;
+template <class OpA, class OpB, bool ROWS_A_CONTIG, bool ROWS_B_CONTIG>
+__global__ void __launch_bounds__(256) sgemm_big(int M, int N, int K, OpA A, OpB B, float *C, int64_t cbs,
+                                                 int64_t crs, int64_t ccs, const float *scale, float beta,
+                                                 const float *C0, int64_t c0bs, int64_t c0rs, int64_t c0cs) {
+  __shared__ __align__(16) float As[BK][BM + 4];
+  __shared__ __align__(16) float Bs[BK][BN + 4];
+  const int b = blockIdx.z, m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  float acc[8][8] = {};
+  float ra[4], rb[4];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;
+      int row, kk;
+      if (ROWS_A_CONTIG) { row = e & 127; kk = e >> 7; } else { row = e >> 3; kk = e & 7; }
+      ra[q] = (m0 + row < M && k0 + kk < K) ? A(b, m0 + row, k0 + kk) : 0.f;
+      int col, kb;
+      if (ROWS_B_CONTIG) { kb = e & 7; col = e >> 3; } else { kb = e >> 7; col = e & 127; }
+      rb[q] = (n0 + col < N && k0 + kb < K) ? B(b, k0 + kb, n0 + col) : 0.f;
+    }
+  };
+  auto store = [&]() {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;
+      int row, kk;
+      if (ROWS_A_CONTIG) { row = e & 127; kk = e >> 7; } else { row = e >> 3; kk = e & 7; }
+      As[kk][row] = ra[q];
+      int col, kb;
+      if (ROWS_B_CONTIG) { kb = e & 7; col = e >> 3; } else { kb = e >> 7; col = e & 127; }
+      Bs[kb][col] = rb[q];
+    }
+  };
+  load(0);
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    store();
+    __syncthreads();
+    if (k0 + BK < K) load(k0 + BK);   // next step's operands in flight during this step's FFMAs
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4 *>(&As[kk][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4 *>(&As[kk][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[kk][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[kk][64 + tx * 4]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[u][v] = fmaf(av[u], bv[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+  const float sc = scale ? scale[b] : 1.f;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int i = m0 + (u < 4 ? ty * 4 + u : 64 + ty * 4 + u - 4);
+    if (i >= M) continue;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int j = n0 + (v < 4 ? tx * 4 + v : 64 + tx * 4 + v - 4);
+      if (j >= N) continue;
+      float o = sc * acc[u][v];
+      if (C0) o = fmaf(beta, C0[b * c0bs + i * c0rs + j * c0cs], o);
+      C[b * cbs + i * crs + j * ccs] = o;
+    }
+  }
+}
+
 template <bool RA, bool RB, class OpA, class OpB>
 lcae_status gemm(lcae_layer *L, int batch, int M, int N, int K, OpA A, OpB B, float *C, int64_t cbs, int64_t crs,
                  int64_t ccs, const float *scale = nullptr, float beta = 0.f, const float *C0 = nullptr,
                  int64_t c0bs = 0, int64_t c0rs = 0, int64_t c0cs = 0) {
+  if (M >= BM && N >= BN) {
+    dim3 grid(cdiv(N, BN), cdiv(M, BM), batch);
+    sgemm_big<OpA, OpB, RA, RB><<<grid, 256, 0, L->st>>>(M, N, K, A, B, C, cbs, crs, ccs, scale, beta, C0, c0bs,
+                                                        c0rs, c0cs);
+    LCAE_CK_LAUNCH(L);
+    return LCAE_OK;
+  }
   dim3 grid(cdiv(N, TN), cdiv(M, TM), batch);
   sgemm_batched<OpA, OpB, RA, RB><<<grid, 256, 0, L->st>>>(M, N, K, A, B, C, cbs, crs, ccs, scale, beta, C0, c0bs,
                                                           c0rs, c0cs);
