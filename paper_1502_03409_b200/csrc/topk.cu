@@ -20,8 +20,13 @@ __global__ void topk_init_kernel(float *vals, int32_t *ids, int64_t n) {
   }
 }
 
+// KT: the state length as a compile-time constant (the common K = 1..8, 16, 32: insertion and register arrays sized
+// exactly), or KMAX with the runtime K masking the rest
+template <int KT>
 __global__ void __launch_bounds__(128) topk_update_kernel(const float *__restrict__ act, int64_t m, int64_t units,
-                                                          int K, int64_t id0, float *vals, int32_t *ids) {
+                                                          int K_, int64_t id0, float *vals, int32_t *ids) {
+  const int K = KT < KMAX ? KT : K_;
+  constexpr int KMAX = KT;
   const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u >= units) return;
   float v[KMAX];
@@ -95,7 +100,16 @@ extern "C" lcae_status lcae_topk_update(const float *act, int64_t m, int64_t uni
     return LCAE_ERR_ARG;
   }
   if (m == 0 || units == 0) return LCAE_OK;
-  topk_update_kernel<<<(unsigned)((units + 127) / 128), 128, 0, (cudaStream_t)stream>>>(act, m, units, K, id0, vals, ids);
+  const unsigned blocks = (unsigned)((units + 127) / 128);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (K) {
+#define LCAE_TOPK(KV) \
+  case KV: topk_update_kernel<KV><<<blocks, 128, 0, st>>>(act, m, units, K, id0, vals, ids); break;
+    LCAE_TOPK(1) LCAE_TOPK(2) LCAE_TOPK(3) LCAE_TOPK(4) LCAE_TOPK(5) LCAE_TOPK(6) LCAE_TOPK(7) LCAE_TOPK(8)
+    LCAE_TOPK(16)
+#undef LCAE_TOPK
+    default: topk_update_kernel<KMAX><<<blocks, 128, 0, st>>>(act, m, units, K, id0, vals, ids); break;
+  }
   LCAE_CK(cudaGetLastError());
   return LCAE_OK;
 }
