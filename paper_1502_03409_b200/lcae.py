@@ -77,14 +77,8 @@ def _load():
         "lcae_profile_read": (C.c_int, [P, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
         "lcae_last_error": (C.c_char_p, []),
         "lcae_version": (C.c_char_p, []),
-        "lcae_dev_umma_selftest": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P]),
-        "lcae_dev_tma_selftest": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P]),
-        "lcae_dev_red_probe": (C.c_int, [P, C.c_int64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
-        "lcae_dev_tmem_shape_selftest": (C.c_int, [P]),
     }
     for name, (res, args) in sigs.items():
-        if name.startswith("lcae_dev_") and not hasattr(lib, name):
-            continue   # dev hooks are optional (A/B of older builds via LCAE_LIB)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
@@ -92,6 +86,37 @@ def _load():
 
 
 lib = _load()
+
+_devlib = None
+
+
+def devlib():
+    """liblcae_dev.so: the product library plus the hardware self-tests / micro-benchmarks (lcae_dev_*), which
+    the product library does not carry."""
+    global _devlib
+    if _devlib is None:
+        path = os.path.join(_HERE, "liblcae_dev.so")
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not built (make -C paper_1502_03409_b200/csrc)")
+        d = C.CDLL(path)
+        P = C.c_void_p
+        for name, (res, args) in {
+            "lcae_dev_umma_selftest": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P]),
+            "lcae_dev_tma_selftest": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P]),
+            "lcae_dev_red_probe": (C.c_int, [P, C.c_int64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
+            "lcae_dev_tmem_shape_selftest": (C.c_int, [P]),
+            "lcae_last_error": (C.c_char_p, []),
+        }.items():
+            fn = getattr(d, name)
+            fn.restype = res
+            fn.argtypes = args
+        _devlib = d
+    return _devlib
+
+
+def dev_check(status: int):
+    if status != LCAE_OK:
+        raise LcaeError(status, devlib().lcae_last_error().decode())
 
 # Every symbol include/lcae.h declares (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("lcae_config_default", "lcae_geometry", "lcae_create", "lcae_destroy", "lcae_set_params",

@@ -25,7 +25,7 @@ def test_umma_descriptors(torch_cuda, a_mn, b_mn, N, K):
     A = torch.randn(128, K, generator=g).to(torch.bfloat16).cuda()
     B = torch.randn(K, N, generator=g).to(torch.bfloat16).cuda()
     D = torch.zeros(128, N, dtype=torch.float32, device="cuda")
-    lcae.check(lcae.lib.lcae_dev_umma_selftest(a_mn, b_mn, N, K, 0, A.data_ptr(), B.data_ptr(), D.data_ptr()))
+    lcae.dev_check(lcae.devlib().lcae_dev_umma_selftest(a_mn, b_mn, N, K, 0, A.data_ptr(), B.data_ptr(), D.data_ptr()))
     ref = A.float() @ B.float()
     err = (D - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-5, err
@@ -48,7 +48,7 @@ def test_tma_swizzle_and_oob(torch_cuda):
     src = torch.arange(rows * cols, dtype=torch.float32).reshape(rows, cols).to(torch.bfloat16).cuda()
     for (r0, c0, box) in ((0, 0, 16), (8, 64, 32), (30, 160, 16)):
         dump = torch.zeros(box * 128, dtype=torch.uint8, device="cuda")
-        lcae.check(lcae.lib.lcae_dev_tma_selftest(src.data_ptr(), rows, cols, box, r0, c0, dump.data_ptr()))
+        lcae.dev_check(lcae.devlib().lcae_dev_tma_selftest(src.data_ptr(), rows, cols, box, r0, c0, dump.data_ptr()))
         got = dump.cpu().view(torch.bfloat16).float().numpy().reshape(box, 64)
         full = np.zeros((box, 64), dtype=np.float32)
         s = src.float().cpu().numpy()
@@ -68,7 +68,7 @@ def test_red_probe_reports(torch_cuda, capsys):
     for mode in (0, 1, 2):
         ms = C.c_float()
         reps = 64
-        lcae.check(lcae.lib.lcae_dev_red_probe(buf.data_ptr(), n, reps, mode, 148 * 16, C.byref(ms)))
+        lcae.dev_check(lcae.devlib().lcae_dev_red_probe(buf.data_ptr(), n, reps, mode, 148 * 16, C.byref(ms)))
         elems = 148 * 16 * 256 * reps * (4 if mode == 1 else 1)
         out[mode] = elems / (ms.value * 1e-3) / 1e9
     with capsys.disabled():
@@ -81,8 +81,8 @@ def test_tmem_16x256b_thread_map():
     each 8-column half (the map ptx.cuh documents)."""
     from paper_1502_03409_b200 import lcae
     out = np.zeros((4, 2, 32, 8), dtype=np.uint32)
-    lcae.lib.lcae_dev_tmem_shape_selftest.argtypes = [C.c_void_p]
-    lcae.check(lcae.lib.lcae_dev_tmem_shape_selftest(out.ctypes.data))
+    lcae.devlib().lcae_dev_tmem_shape_selftest.argtypes = [C.c_void_p]
+    lcae.dev_check(lcae.devlib().lcae_dev_tmem_shape_selftest(out.ctypes.data))
     for w in range(4):
         for h in range(2):
             for t in range(32):

@@ -7,7 +7,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1502_03409_b200 import lcae  # noqa: E402
 
-f = lcae.lib.lcae_dev_mma_rate
+f = lcae.devlib().lcae_dev_mma_rate
 f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
 for N in (64, 128, 256):
     for a_mn, b_mn in ((0, 0), (1, 0), (0, 1)):

@@ -1,7 +1,7 @@
 import ctypes as C, numpy as np, torch, sys
 sys.path.insert(0, '/root/repo')
 from paper_1502_03409_b200 import lcae
-lib = lcae.lib
+lib = lcae.devlib()
 lib.lcae_dev_tma_offset_selftest.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
 rows, cols = 100, 128
 src = torch.arange(rows * cols, dtype=torch.float32).reshape(rows, cols).to(torch.bfloat16).cuda()

@@ -9,8 +9,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1502_03409_b200 import lcae  # noqa: E402
 
 out = np.zeros((4, 2, 32, 8), dtype=np.uint32)
-lcae.lib.lcae_dev_tmem_shape_selftest.argtypes = [C.c_void_p]
-lcae.check(lcae.lib.lcae_dev_tmem_shape_selftest(out.ctypes.data))
+lcae.devlib().lcae_dev_tmem_shape_selftest.argtypes = [C.c_void_p]
+lcae.dev_check(lcae.devlib().lcae_dev_tmem_shape_selftest(out.ctypes.data))
 for w in (0, 1):
     for h in (0, 1):
         for t in (0, 1, 2, 3, 4, 5, 31):
