@@ -53,9 +53,26 @@ def alg_bytes(shape):
     return 8.0 * w * (2 if shape.momentum > 0 else 1) + 8.0 * shape.fields * (shape.n + 1) + 2.0 * x + 4.0 * x
 
 
+def uses_gt(shape):
+    """Shapes beyond the fused kernel (k > 128, m > 256, n > 4096) run on the general tcgen05 GEMM path."""
+    return shape.filters > 128 or shape.batch > 256 or -(-shape.n // 64) * 64 > 4096
+
+
+def gt_executed_flops(shape):
+    """FLOPs of the general path's five GEMMs per field with their tile padding (gt_path.cu: 128-row M tiles,
+    BN in {64, 128, 192, 256} columns, 64-deep K steps)."""
+    up = lambda v, t: -(-v // t) * t
+    bn = lambda N: 64 if N <= 64 else 128 if N <= 128 else 192 if N <= 192 else 256
+    g = lambda M, N, K: 2.0 * up(M, 128) * up(N, bn(N)) * up(K, 64)
+    k, n, m = shape.filters, shape.n, shape.batch
+    return (g(k, m, n) + g(n, m, k) + g(k, m, n) + 2 * g(k, n, m) + g(n, m, k)) * shape.fields
+
+
 def executed_flops(shape):
     """FLOPs the tcgen05 MMAs of the fused step kernel execute: filters padded to KP = 128, patch
     rows to 64-row tiles, samples to 128 per CTA, plus the exact -I tiles of the residual and dX products."""
+    if uses_gt(shape):
+        return gt_executed_flops(shape)
     KP, NT, MC = 128, 64, 128
     T = -(-shape.n // NT)
     CB = -(-shape.batch // MC)
@@ -301,8 +318,8 @@ def run_infer(args, shape):
 EXTRA = {"c15b": LayerShape("c15b", 710, 712, 3, 18, 18, 2, 128, 1, 256, lr=1e-3 / 256),
          # SURVEY.md §8(d) c3': the paper-exact layer 1 (16 x 16 x 3 receptive fields, stride 4 ->
          # 4 x 4 x 24 = 384 filters per field; PAPER.md:111 mini-batch 192) on 300 x 300 x 3 images: 72 x 72 =
-         # 5184 fields, 1.53 B weights. k = 384 exceeds the fused bf16 kernel's TMEM budget (k <= 128), so it runs
-         # on the fp32 path (--precision fp32).
+         # 5184 fields, 1.53 B weights. k = 384 exceeds the fused bf16 kernel's TMEM budget (k <= 128): in bf16 it
+         # runs on the general tcgen05 GEMM path (gt_path.cu), in fp32 (--precision fp32) on the FFMA path.
          "c3p": LayerShape("c3p", 300, 300, 3, 16, 16, 4, 384, 1, 192, lr=1e-3 / 192)}
 
 
@@ -492,7 +509,9 @@ def run_ours(args, shape):
                      if hbm_bound else
                      {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
                       "frac": achieved / tc_peak, "traffic": traffic,
-                      "kernel": "lcae::tc::step_kernel", "kernel_ms": kern_avg, "peak_source": tc_src,
+                      "kernel": ("lcae::gt::bgemm (the five tcgen05 GEMMs of the general path, summed)"
+                                 if uses_gt(shape) else "lcae::tc::step_kernel"),
+                      "kernel_ms": kern_avg, "peak_source": tc_src,
                       "frac_of_sustained": achieved / pk["bf16_sus"], "frac_of_burst": achieved / pk["bf16"],
                       "model_flops_per_step": flops, "executed_flops_per_step": executed_flops(shape),
                       "executed_tflops": executed_flops(shape) / world / (kern_avg * 1e-3) / 1e12,
@@ -586,7 +605,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + sorted(EXTRA) + ["c5fit", "paper3"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"],
-                    help="bf16: the tcgen05 path (default); fp32: the FFMA path (needed for k > 128, e.g. c3p)")
+                    help="bf16: the tcgen05 paths (default; the fused kernel, or the general GEMM path for k > 128, e.g. "
+                         "c3p); fp32: the FFMA path")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of oracle work per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")

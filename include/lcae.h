@@ -17,7 +17,9 @@
  *
  * Precision: LCAE_FP32 computes every product and sum in fp32 (FFMA, no TF32) with an fp64 loss sum;
  * LCAE_BF16 feeds bf16 operands (x, W, h, delta, D rounded RN-even) to tcgen05 tensor cores with fp32
- * accumulation (TMEM), fp32 epilogues and fp32 master weights.
+ * accumulation (TMEM), fp32 epilogues and fp32 master weights. A bf16 layer runs on one fused step kernel
+ * when k <= 128, m <= 256 and n <= 4096; larger layers (e.g. the paper's own layer 1, k = 384)
+ * run the same step as five batched tcgen05 GEMMs with epilogue kernels (same operand rounding).
  *
  * Conventions
  *  - All functions return lcae_status; on error, lcae_last_error() (thread-local, library-owned
@@ -146,7 +148,8 @@ lcae_status lcae_mp_fields(lcae_layer *L, int32_t *n_interior, int32_t *n_bounda
 /* Create a layer on the current CUDA device: validates cfg (as lcae_geometry), allocates parameters,
  * gradient/optimizer state and scratch, and initialises W to unit rows from a counter-based generator,
  * alpha = alpha_init, b = 0 (callers normally overwrite them with lcae_set_params).
- * *out receives the handle. Errors: CONFIG, CUDA (e.g. out of memory), ARG. */
+ * *out receives the handle. Errors: CONFIG (also: a model-parallel bf16 layer beyond the fused kernel's
+ * k <= 128 / m <= 256 / n <= 4096), CUDA (e.g. out of memory), ARG. */
 lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out);
 
 /* Release everything the handle owns. NULL-safe. Synchronises the layer's stream first. */
@@ -240,7 +243,8 @@ lcae_status lcae_region_add(void *stream, float *dst, int32_t dst_h, int32_t dst
 int32_t lcae_last_launch_count(lcae_layer *L);
 
 /* Kernel timing for roofline accounting: enable = 1 starts recording CUDA events (on the layer's stream)
- * around the dominant fused step kernel of every subsequent lcae_step (up to 4096 steps); enable = 0 stops.
+ * around the dominant fused step kernel of every subsequent lcae_step (on the general bf16 path, layers with
+ * k > 128 / m > 256 / n > 4096: around each of its tcgen05 GEMM launches; up to 4096 ranges); enable = 0 stops.
  * lcae_profile_read synchronises and returns the summed duration (ms) and the number of recorded launches,
  * then clears the record. Events add no synchronisation inside the step. */
 lcae_status lcae_profile(lcae_layer *L, int32_t enable);

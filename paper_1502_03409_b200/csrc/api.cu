@@ -194,6 +194,7 @@ lcae_status lcae_destroy(lcae_layer *L) {
   mp_free(L);
   f32_free(L);
   tc_free(L);
+  gt_free(L);
   for (void *p : {(void *)L->W, (void *)L->sigma, (void *)L->alpha, (void *)L->b, (void *)L->vW, (void *)L->va,
                   (void *)L->vb, (void *)L->Wb, (void *)L->x_stage, (void *)L->xt32, (void *)L->xt16,
                   (void *)L->dxt, (void *)L->dx_nhwc, (void *)L->pooled, (void *)L->gW, (void *)L->galpha,
@@ -299,7 +300,20 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
     CKF(dmalloc(L, &L->xt16, mp * img * 2));
     CKF(cudaMemset(L->xt16, 0, mp * img * 2));   // padded batch columns stay zero
     CKF(dmalloc(L, &L->rowsq, F * k * 4));
-    FAIL(tc_alloc(L));
+    // shapes beyond the fused kernel (k > 128, n > 4096, m > 256) take the general tcgen05 GEMM path (gt_path.cu);
+    // LCAE_DEV_FORCE_GT=1 selects it for any shape (test hook: the oracle checks it at small sizes)
+    const char *e = getenv("LCAE_DEV_FORCE_GT");
+    if (tc_unsupported(g) || (e && atoi(e))) {
+      if (cfg->world_size > 1 || cfg->nccl_id) {
+        set_error(std::string("model parallelism needs the fused bf16 kernel: ") +
+                  (tc_unsupported(g) ? tc_unsupported(g) : "LCAE_DEV_FORCE_GT set"));
+        lcae_destroy(L);
+        return LCAE_ERR_CONFIG;
+      }
+      FAIL(gt_alloc(L));
+    } else {
+      FAIL(tc_alloc(L));
+    }
   }
   // model parallel: world_size > 1; or one rank with an NCCL id (the whole layer as a single tile: exercises the
   // communicator, the interior / boundary launches and the loss all-reduce on one GPU)
@@ -406,6 +420,7 @@ static lcae_status run(lcae_layer *L, const float *x, bool update, float *dx, fl
       if ((s = mp_phase(L, ph, update, pooled != nullptr))) return s;
   } else {
     s = (L->cfg.precision == LCAE_FP32) ? f32_step(L, update, pooled != nullptr)
+        : L->gt                          ? gt_step(L, update, pooled != nullptr, encode_only)
                                          : tc_step(L, update, pooled != nullptr, encode_only);
     if (s) return s;
     if ((s = launch_loss_reduce(L, update))) return s;
@@ -516,7 +531,7 @@ lcae_status lcae_sync(lcae_layer *L) {
 lcae_status lcae_field_losses(lcae_layer *L, double *out) {
   if (!L || !out) { set_error("NULL argument"); return LCAE_ERR_ARG; }
   const Geo &g = L->geo;
-  const bool tcp = L->cfg.precision == LCAE_BF16;
+  const bool tcp = L->tc != nullptr;   // the fused kernel keeps one partial per CTA of a cluster
   const int per = tcp ? tc_loss_count(L) / g.F : 1;   // partials per field (CTAs of a cluster)
   double *part = tcp ? tc_loss_part(L) : L->loss_part;
   double *h = nullptr;

@@ -239,7 +239,7 @@ lcae_status launch_hwcn_to_nhwc_f32(lcae_layer *L, const float *xt, float *x) {
 }
 
 lcae_status launch_loss_reduce(lcae_layer *L, bool update) {
-  const bool tcp = L->cfg.precision == LCAE_BF16;
+  const bool tcp = L->tc != nullptr;
   loss_reduce<<<1, 1024, 0, L->st>>>(tcp ? tc_loss_part(L) : L->loss_part, tcp ? tc_loss_count(L) : L->geo.F,
                                      L->loss_dev, L->step_dev, update ? 1 : 0, L->flags_dev);
   LCAE_CK_LAUNCH(L);
@@ -278,7 +278,7 @@ lcae_status launch_get_W_range(lcae_layer *L, float *Wout, int64_t f0, int64_t n
 
 lcae_status launch_refresh_shadow(lcae_layer *L) {
   if (!L->Wb) return LCAE_OK;
-  shadow_w<<<L->sm_count * 8, 256, 0, L->st>>>(L->geo, 128, L->n_al, L->wp, L->W, L->Wb);
+  shadow_w<<<L->sm_count * 8, 256, 0, L->st>>>(L->geo, L->tc ? 128 : L->geo.k, L->n_al, L->wp, L->W, L->Wb);
   LCAE_CK_LAUNCH(L);
   return LCAE_OK;
 }

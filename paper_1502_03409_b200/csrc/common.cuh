@@ -51,7 +51,8 @@ struct F32Scratch {
   float *db = nullptr;                                          // [Fc][n]
 };
 
-struct TcScratch;   // bf16 tensor-core path (tc_path.cu)
+struct TcScratch;   // bf16 tensor-core path: the fused step kernel (tc_host.cu)
+struct GtScratch;   // bf16 tensor-core path for shapes beyond the fused kernel (gt_path.cu)
 struct MpState;     // model-parallel tile state (mp.cu)
 
 // One rank's tile of a model-parallel layer (mp.cu): field rows [R0, R1) x cols [C0, C1) of the global grid;
@@ -103,6 +104,7 @@ struct lcae_layer {
   int launches = 0;
   lcae::F32Scratch f32;
   lcae::TcScratch *tc = nullptr;
+  lcae::GtScratch *gt = nullptr;   // bf16 layers the fused kernel cannot hold (k > 128, n > 4096, m > 256)
   lcae::MpState *mpst = nullptr;   // model-parallel state (world_size > 1)
   // dev checks (sanitizer substitute, include/lcae.h is unaffected): LCAE_DEV_POISON=1 fills every allocation
   // with 0xFF bytes (NaN) so that a read before write shows up in the results; LCAE_DEV_CANARY=1 pads every
@@ -189,6 +191,17 @@ void tc_free(lcae_layer *L);
 lcae_status tc_step(lcae_layer *L, bool update, bool want_pooled, bool encode_only = false, const int *flist = nullptr,
                     int nfl = 0, bool first = true, bool last = true, int reserve_clusters = 0);
 lcae_status tc_finalize(lcae_layer *L);
+// the fused kernel's limits (NULL = holds): a bf16 layer beyond them runs on the general tcgen05 GEMM path
+const char *tc_unsupported(const Geo &g);
+
+lcae_status gt_alloc(lcae_layer *L);
+void gt_free(lcae_layer *L);
+lcae_status gt_step(lcae_layer *L, bool update, bool want_pooled, bool encode_only);
+
+// shared by the fp32 and the general bf16 paths (f32_path.cu)
+__global__ void col2im_f32(Geo g, int f0, int Fc, const float *dXp, float *dxt);
+__global__ void update_ab_f32(Geo g, int f0, int Fc, float *alpha, float *bvec, const float *da, const float *db,
+                              float *va, float *vb, float lr, float mu, float amin, const int *flags);
 
 // model parallelism (mp.cu)
 lcae_status mp_tile(const lcae_config *c, const Geo &global, int rank, MpTile *t);

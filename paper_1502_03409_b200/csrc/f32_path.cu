@@ -255,35 +255,6 @@ __global__ void __launch_bounds__(256) dcode_f32(Geo g, float *Gm, const float *
   if (threadIdx.x == 0) da[b] = (float)tot;
 }
 
-// Overlap-add by owner gather (deterministic): dxt[y][x][c][i] += sum over fields f in [f0, f0+Fc) covering
-// (y, x) of dXp[f - f0][n(y,x,c,f)][i], fields visited in row-major order.
-__global__ void col2im_f32(Geo g, int f0, int Fc, const float *dXp, float *dxt) {
-  const int64_t total = (int64_t)g.H * g.W * g.C * g.m;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    int i = (int)(t % g.m);
-    int64_t pix = t / g.m;
-    int ch = (int)(pix % g.C);
-    int64_t yx = pix / g.C;
-    int x = (int)(yx % g.W), y = (int)(yx / g.W);
-    int r_lo = y - g.rf_h + 1 <= 0 ? 0 : (y - g.rf_h + g.s) / g.s;
-    int r_hi = min(y / g.s, g.gr - 1);
-    int c_lo = x - g.rf_w + 1 <= 0 ? 0 : (x - g.rf_w + g.s) / g.s;
-    int c_hi = min(x / g.s, g.gc - 1);
-    float acc = 0.f;
-    bool any = false;
-    for (int r = r_lo; r <= r_hi; ++r) {
-      for (int c = c_lo; c <= c_hi; ++c) {
-        int f = r * g.gc + c;
-        if (f < f0 || f >= f0 + Fc) continue;
-        int nrow = ((y - r * g.s) * g.rf_w + (x - c * g.s)) * g.C + ch;
-        acc += dXp[((int64_t)(f - f0) * g.n + nrow) * g.m + i];
-        any = true;
-      }
-    }
-    if (any) dxt[t] += acc;
-  }
-}
-
 // Projected SGD on W rows (fp32 mode keeps W normalised, sigma == 1):
 // v = mu v - lr dW; W' = W + v; W' /= ||W'|| (degenerate rows re-initialised).
 __global__ void __launch_bounds__(256) update_w_f32(Geo g, int f0, float *W, const float *dW, float *vW, float lr,
@@ -327,6 +298,47 @@ __global__ void __launch_bounds__(256) update_w_f32(Geo g, int f0, float *W, con
   for (int t = threadIdx.x; t < n; t += blockDim.x) w[t] *= sc;
 }
 
+__global__ void copy_grads_f32(Geo g, int f0, int Fc, const float *dW, const float *da, const float *db, float *gW,
+                               float *ga, float *gb) {
+  int64_t kn = (int64_t)g.k * g.n, tot = (int64_t)Fc * kn;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    gW[(int64_t)f0 * kn + t] = dW[t];
+    if (t < (int64_t)Fc * g.n) gb[(int64_t)f0 * g.n + t] = db[t];
+    if (t < Fc) ga[f0 + t] = da[t];
+  }
+}
+
+}  // namespace
+
+// Overlap-add by owner gather (deterministic): dxt[y][x][c][i] += sum over fields f in [f0, f0+Fc) covering
+// (y, x) of dXp[f - f0][n(y,x,c,f)][i], fields visited in row-major order.
+__global__ void col2im_f32(Geo g, int f0, int Fc, const float *dXp, float *dxt) {
+  const int64_t total = (int64_t)g.H * g.W * g.C * g.m;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(t % g.m);
+    int64_t pix = t / g.m;
+    int ch = (int)(pix % g.C);
+    int64_t yx = pix / g.C;
+    int x = (int)(yx % g.W), y = (int)(yx / g.W);
+    int r_lo = y - g.rf_h + 1 <= 0 ? 0 : (y - g.rf_h + g.s) / g.s;
+    int r_hi = min(y / g.s, g.gr - 1);
+    int c_lo = x - g.rf_w + 1 <= 0 ? 0 : (x - g.rf_w + g.s) / g.s;
+    int c_hi = min(x / g.s, g.gc - 1);
+    float acc = 0.f;
+    bool any = false;
+    for (int r = r_lo; r <= r_hi; ++r) {
+      for (int c = c_lo; c <= c_hi; ++c) {
+        int f = r * g.gc + c;
+        if (f < f0 || f >= f0 + Fc) continue;
+        int nrow = ((y - r * g.s) * g.rf_w + (x - c * g.s)) * g.C + ch;
+        acc += dXp[((int64_t)(f - f0) * g.n + nrow) * g.m + i];
+        any = true;
+      }
+    }
+    if (any) dxt[t] += acc;
+  }
+}
+
 __global__ void update_ab_f32(Geo g, int f0, int Fc, float *alpha, float *bvec, const float *da, const float *db,
                               float *va, float *vb, float lr, float mu, float amin, const int *flags) {
   if (flags[0] | flags[1]) return;
@@ -343,18 +355,6 @@ __global__ void update_ab_f32(Geo g, int f0, int Fc, float *alpha, float *bvec, 
     }
   }
 }
-
-__global__ void copy_grads_f32(Geo g, int f0, int Fc, const float *dW, const float *da, const float *db, float *gW,
-                               float *ga, float *gb) {
-  int64_t kn = (int64_t)g.k * g.n, tot = (int64_t)Fc * kn;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-    gW[(int64_t)f0 * kn + t] = dW[t];
-    if (t < (int64_t)Fc * g.n) gb[(int64_t)f0 * g.n + t] = db[t];
-    if (t < Fc) ga[f0 + t] = da[t];
-  }
-}
-
-}  // namespace
 
 lcae_status f32_alloc(lcae_layer *L) {
   const Geo &g = L->geo;

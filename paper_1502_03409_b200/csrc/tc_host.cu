@@ -138,13 +138,18 @@ static bool window_pieces(const Geo &g, int r0, int rows, int maxlg, int cap, ui
   return true;
 }
 
+const char *tc_unsupported(const Geo &g) {
+  if (g.k > tc::KP) return "filters per field must be <= 128";
+  if (g.m > 2 * tc::MC) return "batch must be <= 256";
+  if (cdiv(g.n, tc::NT) * tc::NT > tc::MAX_NPAD) return "rf_h*rf_w*C must be <= 4096";
+  if ((int64_t)(g.rf_h - 1) * g.W * g.C + g.RW > (1 << 20)) return "field window spans > 2^20 pixel-features";
+  return nullptr;
+}
+
 lcae_status tc_alloc(lcae_layer *L) {
   const Geo &g = L->geo;
-  if (g.k > tc::KP) { set_error("bf16 path: filters per field must be <= 128"); return LCAE_ERR_CONFIG; }
-  if (g.m > 2 * tc::MC) { set_error("bf16 path: batch must be <= 256"); return LCAE_ERR_CONFIG; }
+  if (const char *why = tc_unsupported(g)) { set_error(std::string("bf16 fused kernel: ") + why); return LCAE_ERR_CONFIG; }
   const int T = cdiv(g.n, tc::NT);
-  if (T * tc::NT > tc::MAX_NPAD) { set_error("bf16 path: rf_h*rf_w*C must be <= 4096"); return LCAE_ERR_CONFIG; }
-  if ((int64_t)(g.rf_h - 1) * g.W * g.C + g.RW > (1 << 20)) { set_error("bf16 path: field window spans > 2^20 pixel-features"); return LCAE_ERR_CONFIG; }
   TcScratch *s = new TcScratch();
   L->tc = s;
   s->CB = cdiv(g.m, tc::MC);
