@@ -31,7 +31,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-from paper_1502_03409_b200.inputs import CONFIGS, LayerShape, make_images, make_params, stratified_fields  # noqa: E402
+from paper_1502_03409_b200.inputs import (CONFIGS, EXTRA_CONFIGS, LayerShape, make_images, make_params,  # noqa: E402
+                                          stratified_fields)
 
 METRIC = "images/sec per LC-autoencoder training step"
 
@@ -315,12 +316,7 @@ def run_infer(args, shape):
 # SURVEY.md §8(d) c5 "15 B point": the paper's parameter count ("15 billion parameters") as one
 # c3-shaped layer, 347 x 348 fields of 18 x 18 x 3 -> 128 filters (15.02 B weights), batch 256, on ONE GPU
 # (fp32 master + bf16 shadow ~ 6 B/param = 90 GB of the 180 GB HBM). Weights are initialised on the device.
-EXTRA = {"c15b": LayerShape("c15b", 710, 712, 3, 18, 18, 2, 128, 1, 256, lr=1e-3 / 256),
-         # SURVEY.md §8(d) c3': the paper-exact layer 1 (16 x 16 x 3 receptive fields, stride 4 ->
-         # 4 x 4 x 24 = 384 filters per field; PAPER.md:111 mini-batch 192) on 300 x 300 x 3 images: 72 x 72 =
-         # 5184 fields, 1.53 B weights. k = 384 exceeds the fused bf16 kernel's TMEM budget (k <= 128): in bf16 it
-         # runs on the general tcgen05 GEMM path (gt_path.cu), in fp32 (--precision fp32) on the FFMA path.
-         "c3p": LayerShape("c3p", 300, 300, 3, 16, 16, 4, 384, 1, 192, lr=1e-3 / 192)}
+EXTRA = dict(EXTRA_CONFIGS)   # c15b, c3p (inputs.py); k = 384 (c3p) runs on the general tcgen05 GEMM path in bf16
 
 
 FP32_ALU_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 TFLOP/s of FFMA at the 1965 MHz maximum SM clock

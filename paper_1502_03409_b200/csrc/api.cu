@@ -253,7 +253,13 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
   CKF(cudaDeviceGetAttribute(&L->sm_count, cudaDevAttrMultiProcessorCount, L->device));
   const size_t F = g.F, k = g.k, n = g.n, m = g.m, img = (size_t)g.H * g.W * g.C;
   L->n_al = (int)((n + 7) / 8 * 8);
-  L->wp = cfg->precision == LCAE_FP32 ? (int)n : L->n_al;   // fp32 master row pitch (16-byte rows, bf16)
+  // bf16 shapes beyond the fused kernel (k > 128, n > 4096, m > 256) take the general tcgen05 GEMM path (gt_path.cu);
+  // LCAE_DEV_FORCE_GT=1 selects it for any shape (test hook: the oracle checks it at small sizes)
+  const char *force_gt = getenv("LCAE_DEV_FORCE_GT");
+  const bool use_gt = cfg->precision == LCAE_BF16 && (tc_unsupported(g) || (force_gt && atoi(force_gt)));
+  // fp32 master row pitch: n (fp32 path), 16-byte rows (fused kernel), 128-byte rows (general path: its SGD epilogue
+  // reads 32-column runs)
+  L->wp = cfg->precision == LCAE_FP32 ? (int)n : use_gt ? (int)((n + 31) / 32 * 32) : L->n_al;
   const size_t wp = L->wp;
   CKF(dmalloc(L, &L->W, F * k * wp * 4));
   CKF(cudaMemsetAsync(L->W, 0, F * k * wp * 4, L->st));
@@ -300,10 +306,7 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
     CKF(dmalloc(L, &L->xt16, mp * img * 2));
     CKF(cudaMemset(L->xt16, 0, mp * img * 2));   // padded batch columns stay zero
     CKF(dmalloc(L, &L->rowsq, F * k * 4));
-    // shapes beyond the fused kernel (k > 128, n > 4096, m > 256) take the general tcgen05 GEMM path (gt_path.cu);
-    // LCAE_DEV_FORCE_GT=1 selects it for any shape (test hook: the oracle checks it at small sizes)
-    const char *e = getenv("LCAE_DEV_FORCE_GT");
-    if (tc_unsupported(g) || (e && atoi(e))) {
+    if (use_gt) {
       if (cfg->world_size > 1 || cfg->nccl_id) {
         set_error(std::string("model parallelism needs the fused bf16 kernel: ") +
                   (tc_unsupported(g) ? tc_unsupported(g) : "LCAE_DEV_FORCE_GT set"));

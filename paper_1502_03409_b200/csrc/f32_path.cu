@@ -312,9 +312,12 @@ __global__ void copy_grads_f32(Geo g, int f0, int Fc, const float *dW, const flo
 
 // Overlap-add by owner gather (deterministic): dxt[y][x][c][i] += sum over fields f in [f0, f0+Fc) covering
 // (y, x) of dXp[f - f0][n(y,x,c,f)][i], fields visited in row-major order.
+// Only the band of image rows the chunk's fields cover is visited (fields are chunked in row-major order).
 __global__ void col2im_f32(Geo g, int f0, int Fc, const float *dXp, float *dxt) {
-  const int64_t total = (int64_t)g.H * g.W * g.C * g.m;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+  const int y0 = (f0 / g.gc) * g.s, y1 = min(g.H, ((f0 + Fc - 1) / g.gc) * g.s + g.rf_h);
+  const int64_t base = (int64_t)y0 * g.W * g.C * g.m, total = (int64_t)(y1 - y0) * g.W * g.C * g.m;
+  for (int64_t tt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; tt < total; tt += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = base + tt;
     int i = (int)(t % g.m);
     int64_t pix = t / g.m;
     int ch = (int)(pix % g.C);

@@ -1,44 +1,75 @@
 // gt_path.cu — the general bf16 tensor-core path: layers the fused step kernel cannot hold (k > 128 filters, n > 4096,
 // m > 256; the paper's own layer 1, c3', has k = 384: PAPER.md:95) run the step as five batched tcgen05 GEMMs with
-// small epilogue kernels between them. Same step, same notation as f32_path.cu (PAPER.md:88 / DESIGN.md R1-R11), same
-// operand rounding as the fused kernel (bf16 x, W, h, delta, alpha D; fp32 accumulation, fp32 master W):
-//   U  = W X_f                      (k x m)   GEMM 1          h = alpha U, s_G, p, J_s    (gt_pool)
-//   R  = W^T h                      (n x m)   GEMM 2          delta = 2(R + b - x), J_r, db (gt_resid)
-//   G  = W delta                    (k x m)   GEMM 3          D = G + lambda h / s, dalpha (gt_dcode)
-//   dW = h delta^T + (alpha D) X^T  (k x n)   GEMM 4 (two K segments into one accumulator)
-//   dXp = W^T (alpha D) - delta     (n x m)   GEMM 5 (epilogue subtracts delta) -> overlap-add into dX (col2im_f32)
-//   projected SGD (gt_update_w: fp32 master + bf16 shadow; update_ab_f32).
-// The GEMM kernel `bgemm` is persistent (one CTA per SM): warp 0 issues TMA loads of 128 x 64 A and BN x 64 B tiles
-// (SW128, 4-stage ring, zero-filled ragged tails), warp 1 issues tcgen05.mma into one of two TMEM accumulators, warps
-// 2-5 drain the other accumulator (tcgen05.ld) to global memory while the next tile's MMAs run.
+// their epilogues doing the element-wise work. Same step, same notation as f32_path.cu (PAPER.md:88 / DESIGN.md
+// R1-R11), same operand rounding and the same lazy projection as the fused kernel (bf16 x, W~, sigma h, delta,
+// sigma alpha D; fp32 accumulation; fp32 master W~ with per-row scale sigma, W = sigma (.) W~):
+//   U  = sigma (.) W~ X_f           (k x m)   GEMM 1, epilogue: h = alpha U, sigma h (bf16), s_G, p, J_s partials
+//   R  = W~^T (sigma h)             (n x m)   GEMM 2, epilogue: delta = 2(R + b - x) (bf16), J_r, db partials
+//   G  = sigma (.) W~ delta         (k x m)   GEMM 3, epilogue: D = G + lambda h / s, sigma alpha D (bf16), dalpha
+//   dXp = W~^T (sigma alpha D) - delta (n x m) GEMM 5, epilogue subtracts delta -> overlap-add into dX (gt_col2im)
+//   sigma dW = (sigma h) delta^T + (sigma alpha D) X^T (k x n) GEMM 4 (two K segments into one accumulator),
+//            epilogue: W~' = W~ - (lr / sigma^2) acc (master + bf16 shadow, TMA stores), ||W~'||^2 row partials;
+//   gt_finalize: sigma' = 1 / ||W~'||, degenerate rows; update_ab_f32: alpha, b.
+// Only U, dXp and the bf16 operands are written between the GEMMs (fixed-order partial sums, reduced per field by
+// gt_parts / gt_finalize: deterministic).
 #include "common.cuh"
 #include "ptx.cuh"
 #include "tma_host.cuh"
 
 #include <algorithm>
+#include <cfloat>
 
 namespace lcae {
 namespace gt {
 
-constexpr int BM = 128, BK = 64, ST = 4;
+constexpr int BM = 128, BK = 64;
+constexpr int stages(int BN) { return BN >= 192 ? 3 : 4; }   // operand ring depth (shared memory: + 64 KB staging)
+constexpr int smem_bytes(int BN) { return stages(BN) * (BM * BK * 2 + BN * BK * 2) + 4 * 16384 + 1024; }
+
+// Epilogue modes: the per-element work between the GEMMs runs on the accumulator tile while it is in registers.
+// POOLP: POOL + the pooled code p; SGD / SGDF: the projected SGD of W~ on the dW accumulator (lean / with momentum or
+// kept gradients).
+enum { EPI_PLAIN = 0, EPI_POOL = 1, EPI_RESID = 2, EPI_DCODE = 3, EPI_SUB16 = 4, EPI_POOLP = 5, EPI_SGD = 6, EPI_SGDF = 7 };
 
 struct GemmArgs {
   CUtensorMap tmA[2], tmB[2];
   int bA[2], bB[2];   // batch-coordinate offset of each operand map (W maps: the chunk's first field)
   int nseg, M, N, K, batch;
-  float *C;
-  int64_t cbs, crs;   // C[b][i][j] at C + b cbs + i crs + j (cbs, crs multiples of 4)
-  const float *C0;    // optional addend: C = acc + beta C0 (same layout as C)
-  float beta;
+  CUtensorMap tmC, tmO;   // store maps of C (fp32, box 32 x 32) and O16 (bf16, box 64 x 32), 128B swizzle
+  float *C;           // fp32 output (PLAIN, SUB16, POOL: U)
+  int64_t cbs, crs;   // C[b][i][j] at C + b cbs + i crs + j (cbs, crs multiples of 8); every per-element side
+                      // buffer below (bf16 or fp32) has this layout
+  // epilogue operands
+  int f0, g, gr, gc;  // chunk's first field; pooling group; field grid
+  float lam, eps;
+  const float *alpha, *bvec, *U;         // alpha [F], b [F][n] (RESID), U (DCODE)
+  const __nv_bfloat16 *I16;              // x (RESID) or delta (SUB16)
+  __nv_bfloat16 *O16;                    // h (POOL), delta (RESID), alpha D (DCODE)
+  float *pooled;                         // p [m][gr][gc][k/g] (POOL, nullable)
+  double *part;                          // per (b, M tile, N tile, warp) partial: sum s, sum e^2, sum D.U
+  float *dbp;                            // db (RESID) / ||W~'||^2 (SGD) row partials [b][N tiles][M]
+  int sb;                                // batch-coordinate offset of the stores (SGD: the chunk's first field)
+  // row scales and SGD operands: W = sigma (.) W~ (the bf16 shadow holds W~); the dW accumulator holds sigma dJ/dW
+  const float *sigma;                    // [F][k]
+  const float *W;                        // W~ master [F][k][wp] (SGD side input)
+  float *vW, *gW;                        // velocity, kept gradient (SGDF; nullable)
+  int64_t wp;
+  float lr, mu;
+  const int *flags;                      // sticky error flags: set -> no parameter writes
 };
 
 // C[b] (M x N, fp32) = sum over segments of A_s[b] (M x K) B_s[b] (K x N); A K-major ([M][K] in global) or
 // MN-major ([K][M]); B K-major ([N][K]) or MN-major ([K][N]). Canonical SW128 layouts as in tc_kernel.cuh
 // (descriptor conventions pinned by tests/test_gpu_selftest.py).
-template <bool AMN, bool BMN, int BN>
+template <bool AMN, bool BMN, int BN, int EPI>
 __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs P) {
+  constexpr int ST = stages(BN);
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
   constexpr uint32_t TCOLS = 2 * BN <= 256 ? 256 : 512;
+  constexpr bool POOLING = EPI == EPI_POOL || EPI == EPI_POOLP;
+  constexpr bool SGD = EPI == EPI_SGD || EPI == EPI_SGDF;
+  constexpr bool st32 = EPI == EPI_PLAIN || EPI == EPI_SUB16 || POOLING || SGD;   // fp32 output (C / W~ master)
+  constexpr bool st16 = POOLING || EPI == EPI_RESID || EPI == EPI_DCODE || SGD;   // bf16 output (O16 / shadow)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[ST], empty[ST], tfull[2], tempty[2];
@@ -112,47 +143,209 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
         ptx::umma_commit(&tfull[buf]);
       }
     }
-  } else {   // epilogue: warp w drains TMEM lanes [32 (w % 4), +32) = rows of the tile
-    const int q = warp & 3;
-    uint32_t tc = 0;
+  } else {
+    // Epilogue: warp w drains TMEM lanes [32 (w % 4), +32) = rows of the tile, 32 columns at a time; results go
+    // through this warp's 128B-swizzled staging boxes (two fp32 32 x 32, two bf16 32 x 64: double-buffered) and
+    // leave by TMA tensor stores (ragged rows / columns clipped by the tensor bounds).
+    const int q = warp & 3, ew = warp - 2, sw = lane & 7;
+    uint8_t *stg = smem + ST * STAGE + ew * 16384;   // [0, 8K): fp32 boxes, [8K, 16K): bf16 boxes
+    uint32_t tc = 0, nchunk = 0, nbox = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tc) {
-      const int b = tile / per, r = tile - b * per, m0 = (r / nt) * BM, n0 = (r % nt) * BN;
+      const int b = tile / per, r = tile - b * per, mi = r / nt, ni = r % nt, m0 = mi * BM, n0 = ni * BN;
       const uint32_t buf = tc & 1;
-      ptx::mbar_wait(&tfull[buf], (tc >> 1) & 1);
-      ptx::tc_fence_after();
-      const int i = m0 + 32 * q + lane;
-      float *crow = P.C + b * P.cbs + (int64_t)i * P.crs;
-      const float *c0row = P.C0 ? P.C0 + b * P.cbs + (int64_t)i * P.crs : nullptr;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        if (n0 + c >= P.N) break;   // warp-uniform
-        float v[16];
-        ptx::tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + buf * BN + c, v);
-        ptx::tmem_ld_wait();
-        if (i < P.M) {
-          const int j0 = n0 + c;
-          if (j0 + 16 <= P.N) {
+      const int row0 = m0 + 32 * q, i = row0 + lane, f = P.f0 + b;
+      const bool rv = i < P.M;
+      // this row's offset in the side inputs (rows past M read row M - 1 and are masked; the sample pitch is a
+      // multiple of 32, so a 32-column chunk never leaves its row)
+      const int64_t ro = b * P.cbs + (int64_t)(rv ? i : P.M - 1) * P.crs;
+      const float a = (POOLING || EPI == EPI_DCODE) ? P.alpha[f] : 0.f;
+      const float brow = (EPI == EPI_RESID && rv) ? P.bvec[(int64_t)f * P.M + i] : 0.f;
+      const float sgr = (POOLING || EPI == EPI_DCODE || SGD) && rv ? P.sigma[(int64_t)f * P.M + i] : 1.f;
+      const int64_t wrow = ((int64_t)f * P.M + (rv ? i : P.M - 1)) * P.wp;   // W~ master row (SGD)
+      const bool frozen = SGD && (P.flags[0] | P.flags[1]);
+      double part = 0.0;
+      float dbs = 0.f;
+      // per-element side input (x / delta in bf16, U or W~ in fp32), loaded one 32-column chunk ahead in registers:
+      // the first chunk's loads are in flight while the accumulator is still being computed
+      constexpr bool has_in = EPI == EPI_RESID || EPI == EPI_SUB16 || EPI == EPI_DCODE || SGD;
+      uint32_t raw[has_in ? 32 : 1];
+      auto load_in = [&](int jj) {
+        if constexpr (EPI == EPI_RESID || EPI == EPI_SUB16) {
+          const uint4 *src = reinterpret_cast<const uint4 *>(P.I16 + ro + jj);
 #pragma unroll
-            for (int t = 0; t < 16; t += 4) {
-              float4 o = make_float4(v[t], v[t + 1], v[t + 2], v[t + 3]);
-              if (c0row) {
-                const float4 a = *reinterpret_cast<const float4 *>(c0row + j0 + t);
-                o.x = fmaf(P.beta, a.x, o.x); o.y = fmaf(P.beta, a.y, o.y);
-                o.z = fmaf(P.beta, a.z, o.z); o.w = fmaf(P.beta, a.w, o.w);
-              }
-              *reinterpret_cast<float4 *>(crow + j0 + t) = o;
-            }
-          } else {
+          for (int h = 0; h < 4; ++h) {
+            const uint4 u = src[h];
+            raw[4 * h] = u.x; raw[4 * h + 1] = u.y; raw[4 * h + 2] = u.z; raw[4 * h + 3] = u.w;
+          }
+        } else if constexpr (has_in) {
+          const float4 *src = reinterpret_cast<const float4 *>(SGD ? P.W + wrow + jj : P.U + ro + jj);
 #pragma unroll
-            for (int t = 0; t < 16; ++t)
-              if (j0 + t < P.N) crow[j0 + t] = c0row ? fmaf(P.beta, c0row[j0 + t], v[t]) : v[t];
+          for (int h = 0; h < 8; ++h) {
+            const float4 u = src[h];
+            raw[4 * h] = __float_as_uint(u.x); raw[4 * h + 1] = __float_as_uint(u.y);
+            raw[4 * h + 2] = __float_as_uint(u.z); raw[4 * h + 3] = __float_as_uint(u.w);
           }
         }
+      };
+      if constexpr (has_in) load_in(n0);
+      ptx::mbar_wait(&tfull[buf], (tc >> 1) & 1);
+      ptx::tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32, ++nchunk) {
+        if (n0 + c >= P.N) break;   // warp-uniform
+        const int j0 = n0 + c;
+        float in[32];
+        if constexpr (EPI == EPI_RESID || EPI == EPI_SUB16) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            in[2 * t] = __uint_as_float(raw[t] << 16);
+            in[2 * t + 1] = __uint_as_float(raw[t] & 0xFFFF0000u);
+          }
+        } else if constexpr (has_in) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) in[t] = __uint_as_float(raw[t]);
+        }
+        if constexpr (has_in)
+          if (c + 32 < BN && j0 + 32 < P.N) load_in(j0 + 32);
+        float v[32];
+        ptx::tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + buf * BN + c, v);
+        ptx::tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + buf * BN + c + 16, v + 16);
+        ptx::tmem_ld_wait();
+        uint32_t okm = 0;   // valid columns of this row
+#pragma unroll
+        for (int t = 0; t < 32; ++t) okm |= (rv && j0 + t < P.N) ? 1u << t : 0u;
+        float o[32];        // fp32 result (C) or the value rounded to the bf16 side output
+        if constexpr (EPI == EPI_PLAIN) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) o[t] = v[t];
+        } else if constexpr (EPI == EPI_SUB16) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) o[t] = v[t] - in[t];   // dXp = W^T (alpha D) - delta
+        } else if constexpr (SGD) {
+          // the accumulator holds sigma dJ/dW. Lean: rownorm(sigma W~ - lr dJ/dW) = rownorm(W~ - (lr / sigma^2) acc),
+          // so W~ is updated without the sigma scale and sigma' = 1 / ||W~'|| (gt_finalize); with momentum the
+          // velocity lives in W's scale and W~' = sigma W~ + v (as the fused kernel)
+          const float isg = 1.f / sgr, cr = -P.lr * isg;
+          float rs = 0.f;
+          float vo[32];
+          if constexpr (EPI == EPI_SGDF) {
+            if (P.vW) {
+#pragma unroll
+              for (int t = 0; t < 32; t += 4) {
+                const float4 q4 = *reinterpret_cast<const float4 *>(P.vW + wrow + j0 + t);
+                vo[t] = q4.x; vo[t + 1] = q4.y; vo[t + 2] = q4.z; vo[t + 3] = q4.w;
+              }
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const float acc = (okm >> t & 1) ? v[t] : 0.f;
+            if constexpr (EPI == EPI_SGD) {
+              o[t] = fmaf(cr * isg, acc, in[t]);
+            } else {
+              float upd = cr * acc;
+              if (P.vW) { upd = fmaf(P.mu, vo[t], upd); vo[t] = upd; }
+              o[t] = fmaf(sgr, in[t], upd);
+              v[t] = acc * isg;   // dJ/dW (kept gradient)
+            }
+            rs = fmaf(o[t], o[t], rs);
+          }
+          dbs += rs;
+          if constexpr (EPI == EPI_SGDF) {
+            if (rv && !frozen) {
+#pragma unroll
+              for (int t = 0; t < 32; t += 4) {
+                if (P.vW) *reinterpret_cast<float4 *>(P.vW + wrow + j0 + t) = make_float4(vo[t], vo[t + 1], vo[t + 2], vo[t + 3]);
+                if (P.gW) *reinterpret_cast<float4 *>(P.gW + wrow + j0 + t) = make_float4(v[t], v[t + 1], v[t + 2], v[t + 3]);
+              }
+            }
+          }
+        } else if constexpr (EPI == EPI_RESID) {
+          float jr = 0.f;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {   // e = r + b - x; delta = 2e
+            const float e = (okm >> t & 1) ? v[t] + brow - in[t] : 0.f;
+            jr = fmaf(e, e, jr);
+            o[t] = 2.f * e;
+            dbs += o[t];
+          }
+          part += (double)jr;
+        } else {   // POOL (h = alpha U) or DCODE (D = G + lambda h / s, output alpha D): group sums over g rows
+          float ss[32];
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            v[t] *= sgr;   // U = sigma (.) (W~ X) or G = sigma (.) (W~ delta)
+            const float h = (okm >> t & 1) ? a * (POOLING ? v[t] : in[t]) : 0.f;
+            ss[t] = h * h;
+          }
+          for (int w = 1; w < P.g; w <<= 1)
+#pragma unroll
+            for (int t = 0; t < 32; ++t) ss[t] += __shfl_xor_sync(0xffffffffu, ss[t], w);
+          const bool lead = (lane & (P.g - 1)) == 0;
+          float acc = 0.f;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            if constexpr (POOLING) {
+              const float sg = sqrtf(P.eps + ss[t]);
+              o[t] = sgr * a * v[t];   // sigma h: the decode W^T h = W~^T (sigma h), dW's first term sigma h delta^T
+              if (lead && (okm >> t & 1)) {
+                acc += sg;
+                if constexpr (EPI == EPI_POOLP)
+                  P.pooled[(((int64_t)(j0 + t) * P.gr + f / P.gc) * P.gc + f % P.gc) * (P.M / P.g) + i / P.g] = sg;
+              }
+            } else {
+              // lambda / s_G (as the fused kernel: s_G = 0 only with h = 0, where the product below is 0; R12)
+              const float inv = P.lam * rsqrtf(fmaxf(P.eps + ss[t], 1.17549435e-38f));
+              const float D = (okm >> t & 1) ? fmaf(a * in[t], inv, v[t]) : 0.f;
+              acc = fmaf(D, in[t], acc);   // dalpha = sum D (.) U
+              o[t] = sgr * a * D;   // sigma alpha D (as sigma h above)
+            }
+          }
+          part += (double)acc;
+        }
+        // staging: the chunk's buffers were last read by the store group of chunk nchunk - 2
+        if (lane == 0) ptx::bulk_wait_read1();
+        __syncwarp();
+        if constexpr (st32) {
+          float *sb32 = reinterpret_cast<float *>(stg + (nchunk & 1) * 4096);
+          const float *src = POOLING ? v : o;   // POOL keeps U (fp32) for GEMM 3's epilogue
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            *reinterpret_cast<float4 *>(sb32 + lane * 32 + 4 * (u ^ sw)) =
+                make_float4(src[4 * u], src[4 * u + 1], src[4 * u + 2], src[4 * u + 3]);
+        }
+        const int hb = (c >> 5) & 1;   // 32-column half of the 64-column bf16 box
+        const bool box_done = hb == 1 || n0 + c + 32 >= P.N;
+        if constexpr (st16) {
+          uint8_t *sb16 = stg + 8192 + (nbox & 1) * 4096;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<uint4 *>(sb16 + lane * 128 + 16 * ((4 * hb + u) ^ sw)) =
+                make_uint4(ptx::pack_bf16x2(o[8 * u], o[8 * u + 1]), ptx::pack_bf16x2(o[8 * u + 2], o[8 * u + 3]),
+                           ptx::pack_bf16x2(o[8 * u + 4], o[8 * u + 5]), ptx::pack_bf16x2(o[8 * u + 6], o[8 * u + 7]));
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (!frozen) {
+            if constexpr (st32) ptx::tma_store_3d(&P.tmC, stg + (nchunk & 1) * 4096, j0, row0, P.sb + b);
+            if constexpr (st16)
+              if (box_done) ptx::tma_store_3d(&P.tmO, stg + 8192 + (nbox & 1) * 4096, j0 - 32 * hb, row0, P.sb + b);
+          }
+          ptx::bulk_commit();   // one group per chunk (possibly empty)
+        }
+        if (st16 && box_done) ++nbox;
       }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
+      if constexpr (EPI != EPI_PLAIN && EPI != EPI_SUB16 && !SGD) {   // fixed-order partials (gt_parts sums them)
+        part = warp_sum(part);
+        if (lane == 0) P.part[((int64_t)(b * mt + mi) * nt + ni) * 4 + q] = part;
+      }
+      if ((EPI == EPI_RESID || SGD) && rv) P.dbp[((int64_t)b * nt + ni) * P.M + i] = dbs;
     }
+    if (lane == 0) ptx::bulk_wait0();   // this warp's stores have completed
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -162,18 +355,18 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
   }
 }
 
-template <bool AMN, bool BMN, int BN>
+template <bool AMN, bool BMN, int BN, int EPI>
 lcae_status launch_bn(lcae_layer *L, const GemmArgs &a) {
-  constexpr int smem = ST * (BM * BK * 2 + BN * BK * 2) + 1024;
+  constexpr int smem = smem_bytes(BN);
   static bool attr = false;
   if (!attr) {
-    LCAE_CK(cudaFuncSetAttribute(bgemm<AMN, BMN, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    LCAE_CK(cudaFuncSetAttribute(bgemm<AMN, BMN, BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
   const int tiles = a.batch * cdiv(a.M, BM) * cdiv(a.N, BN);
   const bool prof = L->prof_on && L->prof_n < 4096;   // lcae_profile: events around every GEMM launch
   if (prof) LCAE_CK(cudaEventRecord(L->prof_ev[2 * L->prof_n], L->st));
-  bgemm<AMN, BMN, BN><<<std::min(tiles, L->sm_count), 192, smem, L->st>>>(a);
+  bgemm<AMN, BMN, BN, EPI><<<std::min(tiles, L->sm_count), 192, smem, L->st>>>(a);
   LCAE_CK_LAUNCH(L);
   if (prof) LCAE_CK(cudaEventRecord(L->prof_ev[2 * L->prof_n++ + 1], L->st));
   return LCAE_OK;
@@ -181,13 +374,13 @@ lcae_status launch_bn(lcae_layer *L, const GemmArgs &a) {
 
 inline int pick_bn(int N) { return N <= 64 ? 64 : N <= 128 ? 128 : N <= 192 ? 192 : 256; }
 
-template <bool AMN, bool BMN>
+template <bool AMN, bool BMN, int EPI>
 lcae_status gemm(lcae_layer *L, const GemmArgs &a) {
   switch (pick_bn(a.N)) {
-    case 64: return launch_bn<AMN, BMN, 64>(L, a);
-    case 128: return launch_bn<AMN, BMN, 128>(L, a);
-    case 192: return launch_bn<AMN, BMN, 192>(L, a);
-    default: return launch_bn<AMN, BMN, 256>(L, a);
+    case 64: return launch_bn<AMN, BMN, 64, EPI>(L, a);
+    case 128: return launch_bn<AMN, BMN, 128, EPI>(L, a);
+    case 192: return launch_bn<AMN, BMN, 192, EPI>(L, a);
+    default: return launch_bn<AMN, BMN, 256, EPI>(L, a);
   }
 }
 
@@ -195,156 +388,130 @@ lcae_status gemm(lcae_layer *L, const GemmArgs &a) {
 
 // X_f (n x m) gathered from the HWCN bf16 image into [Fc][n][mp] (16-byte runs; rows of one receptive-field row are
 // consecutive pixel-features).
-__global__ void __launch_bounds__(256) gt_gather(Geo g, int f0, int mp, const __nv_bfloat16 *xt16, __nv_bfloat16 *Xp) {
+__global__ void __launch_bounds__(256) gt_gather(Geo g, int f0, int mp, int mq, const __nv_bfloat16 *xt16,
+                                                 __nv_bfloat16 *Xp) {
   const int b = blockIdx.x, f = f0 + b, r = f / g.gc, c = f - r * g.gc;
-  const int q8 = mp / 8;
+  const int q8 = mq / 8, p8 = mp / 8;   // 16-byte runs per row: destination (pitch mq), source (pitch mp)
   const int64_t rowstride = (int64_t)g.W * g.C;   // pixel-features per image row
   const int64_t base = ((int64_t)r * g.s * rowstride + (int64_t)c * g.s * g.C) * mp;
   const uint4 *src = reinterpret_cast<const uint4 *>(xt16);
-  uint4 *dst = reinterpret_cast<uint4 *>(Xp + (int64_t)b * g.n * mp);
+  uint4 *dst = reinterpret_cast<uint4 *>(Xp + (int64_t)b * g.n * mq);
   for (int t = threadIdx.x; t < g.n * q8; t += blockDim.x) {
     const int row = t / q8, qq = t - row * q8, ry = row / g.RW;
     const int64_t off = base + ((int64_t)ry * rowstride + (row - ry * g.RW)) * mp;
-    dst[t] = src[off / 8 + qq];
+    dst[t] = qq < p8 ? src[off / 8 + qq] : make_uint4(0, 0, 0, 0);
   }
 }
 
-// h = alpha U (bf16 copy for the GEMMs), s_G = sqrt(eps + sum_G h^2) -> p, J_s = lambda sum s, Q = lambda h / s.
-__global__ void __launch_bounds__(256) gt_pool(Geo g, int f0, int mp, const float *U, const float *alpha, float lam,
-                                               float eps, __nv_bfloat16 *H16, float *Q, float *pooled,
-                                               double *loss_part, int enc) {
-  __shared__ double sh[32];
+// Per-field sums of the epilogue partials in a fixed order (deterministic): J_s = lambda sum s (GEMM 1), J_r (GEMM 2),
+// dalpha (GEMM 3), db = sum over N tiles of the per-row partials (GEMM 2).
+__global__ void __launch_bounds__(256) gt_parts(int f0, int n, float lam, const double *P1, int n1, const double *P2,
+                                                int n2, const double *P3, int n3, const float *dbp, int nt2,
+                                                double *loss_part, float *da, float *db, int enc) {
   const int b = blockIdx.x, f = f0 + b;
-  const int k = g.k, m = g.m, gs = g.g, ng = k / gs;
-  const float a = alpha[f];
-  const int64_t kb = (int64_t)b * k * mp;
-  double acc = 0.0;
-  for (int t = threadIdx.x; t < ng * m; t += blockDim.x) {
-    const int G = t / m, i = t - G * m;
-    float ss = 0.f;
-    for (int q = 0; q < gs; ++q) {
-      const float h = a * U[kb + (int64_t)(G * gs + q) * mp + i];
-      ss = fmaf(h, h, ss);
-    }
-    const float s = sqrtf(eps + ss);
-    acc += (double)s;
-    if (pooled) {
-      const int r = f / g.gc, c = f - r * g.gc;
-      pooled[(((int64_t)i * g.gr + r) * g.gc + c) * ng + G] = s;
-    }
-    const float inv = s > 0.f ? lam / s : 0.f;
-    for (int q = 0; q < gs; ++q) {
-      const int64_t o = kb + (int64_t)(G * gs + q) * mp + i;
-      const float h = a * U[o];
-      H16[o] = __float2bfloat16_rn(h);
-      if (Q) Q[o] = h * inv;
-    }
-  }
-  const double tot = block_sum_f64(acc, sh);
   if (threadIdx.x == 0) {
-    loss_part[2 * f + 1] = (double)lam * tot;
-    if (enc) loss_part[2 * f] = 0.0;
-  }
-}
-
-// e = R + b - x (x: the bf16 image value the GEMMs use); J_r = sum e^2; delta = 2e (fp32 in place, bf16 copy);
-// db = sum_i delta. One warp per patch row.
-__global__ void __launch_bounds__(256) gt_resid(Geo g, int f0, int mp, float *R, const float *bvec,
-                                                const __nv_bfloat16 *Xp, __nv_bfloat16 *d16, double *loss_part,
-                                                float *db) {
-  __shared__ double sh[32];
-  const int b = blockIdx.x, f = f0 + b, n = g.n, m = g.m;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int64_t nb = (int64_t)b * n * mp;
-  double acc = 0.0;
-  for (int row = wid; row < n; row += nw) {
-    const float bb = bvec[(int64_t)f * n + row];
-    float dsum = 0.f;
-    for (int i = lane; i < m; i += 32) {
-      const int64_t o = nb + (int64_t)row * mp + i;
-      const float e = R[o] + bb - __bfloat162float(Xp[o]);
-      acc += (double)e * (double)e;
-      const float dl = 2.f * e;
-      R[o] = dl;
-      d16[o] = __float2bfloat16_rn(dl);
-      dsum += dl;
+    double s1 = 0.0;
+    for (int e = 0; e < n1; ++e) s1 += P1[(int64_t)b * n1 + e];
+    loss_part[2 * f + 1] = (double)lam * s1;
+    if (P2) {
+      double s2 = 0.0;
+      for (int e = 0; e < n2; ++e) s2 += P2[(int64_t)b * n2 + e];
+      loss_part[2 * f] = s2;
+    } else if (enc) {
+      loss_part[2 * f] = 0.0;
     }
-    dsum = warp_sum(dsum);
-    if (lane == 0) db[(int64_t)b * n + row] = dsum;
+    if (P3) {
+      double s3 = 0.0;
+      for (int e = 0; e < n3; ++e) s3 += P3[(int64_t)b * n3 + e];
+      da[b] = (float)s3;
+    }
   }
-  const double tot = block_sum_f64(acc, sh);
-  if (threadIdx.x == 0) loss_part[2 * f] = tot;
+  if (P2)
+    for (int row = threadIdx.x; row < n; row += blockDim.x) {
+      float acc = 0.f;
+      for (int t = 0; t < nt2; ++t) acc += dbp[((int64_t)b * nt2 + t) * n + row];
+      db[(int64_t)b * n + row] = acc;
+    }
 }
 
-// D = G + Q; dalpha = sum D (.) U; D16 = bf16(alpha D) (the operand of dW's second term and of dX).
-__global__ void __launch_bounds__(256) gt_dcode(Geo g, int f0, int mp, const float *G, const float *Q, const float *U,
-                                                const float *alpha, __nv_bfloat16 *D16, float *da) {
+// New row scales sigma' = 1 / ||W~'_row|| from the SGD epilogue's row partials (fixed order; PAPER.md:89 unit-norm
+// projection), degenerate rows re-initialised from the counter-based generator (as the fused path).
+__global__ void __launch_bounds__(128) gt_finalize(Geo g, int f0, int nt4, const float *rsqp, float *sigma, float *W,
+                                                   __nv_bfloat16 *Wb, int64_t wp, int n_al, float *vW, uint64_t seed,
+                                                   const int64_t *step_dev, int row0, int col0, int ggc, int *reinit,
+                                                   const int *flags) {
   __shared__ double sh[32];
-  const int b = blockIdx.x, m = g.m;
-  const float a = alpha[f0 + b];
-  const int64_t kb = (int64_t)b * g.k * mp;
-  double acc = 0.0;
-  for (int t = threadIdx.x; t < g.k * m; t += blockDim.x) {
-    const int row = t / m, i = t - row * m;
-    const int64_t o = kb + (int64_t)row * mp + i;
-    const float d = G[o] + Q[o];
-    acc += (double)d * (double)U[o];
-    D16[o] = __float2bfloat16_rn(a * d);
-  }
-  const double tot = block_sum_f64(acc, sh);
-  if (threadIdx.x == 0) da[b] = (float)tot;
-}
-
-// Projected SGD on W rows (W kept unit-norm, sigma == 1, as in the fp32 path): v = mu v - lr dW; W' = W + v;
-// W' /= ||W'|| (degenerate rows re-initialised from the counter-based generator); the bf16 shadow row
-// is rewritten from W'. dW rows have pitch n_al.
-__global__ void __launch_bounds__(256) gt_update_w(Geo g, int f0, int wp, int n_al, float *W, __nv_bfloat16 *Wb,
-                                                   const float *dW, float *vW, float *gW, float lr, float mu,
-                                                   uint64_t seed, const int64_t *step_dev, int row0, int col0, int ggc,
-                                                   int *reinit, const int *flags) {
-  __shared__ double sh[32];
-  __shared__ float s_scale;
-  const int b = blockIdx.x, j = blockIdx.y, f = f0 + b, n = g.n;
-  const float *d = dW + ((int64_t)b * g.k + j) * n_al;
-  const int64_t wo = ((int64_t)f * g.k + j) * wp;
-  if (gW)
-    for (int t = threadIdx.x; t < n; t += blockDim.x) gW[wo + t] = d[t];
-  if (flags[0] | flags[1]) return;   // flagged error: parameters frozen (include/lcae.h "Errors")
-  float *w = W + wo;
-  float *v = vW ? vW + wo : nullptr;
-  double acc = 0.0;
-  for (int t = threadIdx.x; t < n; t += blockDim.x) {
-    float upd = -lr * d[t];
-    if (v) { upd = fmaf(mu, v[t], upd); v[t] = upd; }
-    const float wn = w[t] + upd;
-    w[t] = wn;
-    acc += (double)wn * wn;
-  }
-  const double tot = block_sum_f64(acc, sh);
-  if (threadIdx.x == 0) s_scale = tot < 1e-60 ? -1.f : (float)(1.0 / sqrt(tot));
+  __shared__ int bad[128];
+  __shared__ int nbad;
+  __shared__ float s_inv;
+  if (flags[0] | flags[1]) return;   // flagged step: parameters frozen (include/lcae.h "Errors")
+  const int b = blockIdx.x, f = f0 + b, k = g.k, n = g.n;
+  if (threadIdx.x == 0) nbad = 0;
   __syncthreads();
-  float sc = s_scale;
-  if (sc < 0.f) {
-    const int r = f / g.gc, c = f - r * g.gc;
-    const uint64_t gf = (uint64_t)((row0 + r) * ggc + col0 + c);
-    const uint64_t key = splitmix64(seed ^ ((uint64_t)*step_dev << 40) ^ (gf << 20) ^ (uint64_t)j);
+  for (int r = threadIdx.x; r < k; r += blockDim.x) {
+    float rs = 0.f;
+    for (int t = 0; t < nt4; ++t) rs += rsqp[((int64_t)b * nt4 + t) * k + r];
+    if (!(rs >= FLT_MIN)) {   // R13: squared row norm below the smallest normal float
+      const int slot = atomicAdd(&nbad, 1);
+      if (slot < 128) bad[slot] = r;
+    } else {
+      sigma[(int64_t)f * k + r] = rsqrtf(rs);
+    }
+  }
+  __syncthreads();
+  const int nb = min(nbad, 128);
+  for (int ib = 0; ib < nb; ++ib) {   // rare path
+    const int r = bad[ib];
+    const int fr = f / g.gc, fc = f - fr * g.gc;
+    const uint64_t gf = (uint64_t)((row0 + fr) * ggc + col0 + fc);
+    const uint64_t key = splitmix64(seed ^ ((uint64_t)*step_dev << 40) ^ (gf << 20) ^ (uint64_t)r);
     double a2 = 0.0;
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
       const double u = (double)(splitmix64(key + (uint64_t)t) >> 40) / 16777216.0 - 0.5;
-      w[t] = (float)u;
-      if (v) v[t] = 0.f;
       a2 += u * u;
     }
-    const double tt = block_sum_f64(a2, sh);
-    if (threadIdx.x == 0) { s_scale = (float)(1.0 / sqrt(tt)); atomicAdd(reinit, 1); }
+    const double tot = block_sum_f64(a2, sh);
+    if (threadIdx.x == 0) { s_inv = (float)(1.0 / sqrt(tot)); atomicAdd(reinit, 1); sigma[(int64_t)f * k + r] = 1.f; }
     __syncthreads();
-    sc = s_scale;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const double u = (double)(splitmix64(key + (uint64_t)t) >> 40) / 16777216.0 - 0.5;
+      const float w = (float)u * s_inv;
+      W[((int64_t)f * k + r) * wp + t] = w;
+      Wb[((int64_t)f * k + r) * n_al + t] = __float2bfloat16_rn(w);
+      if (vW) vW[((int64_t)f * k + r) * wp + t] = 0.f;   // a fresh row starts at rest
+    }
+    __syncthreads();
   }
-  __nv_bfloat16 *wb = Wb + ((int64_t)f * g.k + j) * n_al;
-  for (int t = threadIdx.x; t < n; t += blockDim.x) {
-    const float x = w[t] * sc;
-    w[t] = x;
-    wb[t] = __float2bfloat16_rn(x);
+}
+
+// Overlap-add of the chunk's dXp into dX by owner gather (deterministic; fields summed in row-major order): one block
+// per pixel (x, y) of the band of image rows the chunk's fields cover, float4 over (channel, sample), no divisions in
+// the field loop.
+__global__ void __launch_bounds__(128) gt_col2im(Geo g, int mp, int mq, int f0, int Fc, int y0, const float *dXp,
+                                                 float *dxt) {
+  const int y = y0 + blockIdx.y, x = blockIdx.x;
+  const int r_lo = y - g.rf_h + 1 <= 0 ? 0 : (y - g.rf_h + g.s) / g.s, r_hi = min(y / g.s, g.gr - 1);
+  const int c_lo = x - g.rf_w + 1 <= 0 ? 0 : (x - g.rf_w + g.s) / g.s, c_hi = min(x / g.s, g.gc - 1);
+  const int CM = g.C * mp;
+  float *dst = dxt + ((int64_t)y * g.W + x) * CM;
+  for (int e = 4 * threadIdx.x; e < CM; e += 4 * blockDim.x) {
+    const int ch = e / mp, i = e - ch * mp;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool any = false;
+    for (int r = r_lo; r <= r_hi; ++r)
+      for (int c = c_lo; c <= c_hi; ++c) {
+        const int f = r * g.gc + c;
+        if (f < f0 || f >= f0 + Fc) continue;
+        const int nrow = ((y - r * g.s) * g.rf_w + (x - c * g.s)) * g.C + ch;
+        const float4 v = *reinterpret_cast<const float4 *>(dXp + ((int64_t)(f - f0) * g.n + nrow) * mq + i);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        any = true;
+      }
+    if (any) {
+      float4 o = *reinterpret_cast<float4 *>(dst + e);
+      o.x += acc.x; o.y += acc.y; o.z += acc.z; o.w += acc.w;
+      *reinterpret_cast<float4 *>(dst + e) = o;
+    }
   }
 }
 
@@ -358,44 +525,57 @@ __global__ void gt_copy_ab(int f0, int Fc, int n, const float *da, const float *
 }  // namespace gt
 
 struct GtScratch {
-  int Fc = 0;
+  int Fc = 0, mq = 0;   // fields per chunk; sample pitch of the per-field buffers (multiple of 32)
   __nv_bfloat16 *Xp = nullptr, *H16 = nullptr, *d16 = nullptr, *D16 = nullptr;   // [Fc][n|k][mp]
-  float *U = nullptr, *Q = nullptr, *G = nullptr;                               // [Fc][k][mp]
-  float *R = nullptr, *dXp = nullptr;                                           // [Fc][n][mp] (R: r, then delta)
-  float *dW = nullptr;                                                          // [Fc][k][n_al]
+  float *U = nullptr;                                                           // [Fc][k][mp]
+  float *dXp = nullptr;                                                         // [Fc][n][mp]
   float *da = nullptr, *db = nullptr;                                           // [Fc], [Fc][n]
+  double *part[3] = {nullptr, nullptr, nullptr};                                // epilogue partials of GEMMs 1-3
+  int npart[3] = {0, 0, 0};                                                     // per field
+  float *dbp = nullptr;                                                         // [Fc][N tiles][n]
+  float *rsqp = nullptr;                                                        // [Fc][N tiles][k]
+  int nt2 = 0, nt4 = 0;
   gt::GemmArgs ga[5];
 };
 
 lcae_status gt_alloc(lcae_layer *L) {
   const Geo &g = L->geo;
-  const int64_t k = g.k, n = g.n, mp = L->mp, na = L->n_al;
+  // the general path's per-field buffers use a sample pitch mq that is a multiple of 32 (one 32-column epilogue
+  // chunk never leaves its row); the image and dX keep L->mp
+  const int64_t k = g.k, n = g.n, mp = (g.m + 31) / 32 * 32, na = L->n_al;
   if (L->mp % 8 || L->n_al % 8) { set_error("gt path: pitches must be multiples of 8"); return LCAE_ERR_CONFIG; }
-  const int64_t per_field = n * mp * (2 + 4 + 2 + 4) + k * mp * (4 + 2 + 4 + 4 + 2) + k * na * 4 + n * 4 + 4;
+  const int bnm = gt::pick_bn(g.m), bnn = gt::pick_bn(g.n);
+  const int ntm = cdiv(g.m, bnm), mtk = cdiv(g.k, gt::BM), mtn = cdiv(g.n, gt::BM);
+  const int64_t per_field = n * mp * (2 + 2 + 4) + k * mp * (2 + 4 + 2) + k * 4 * (cdiv(g.n, bnn) + 1) + n * 4 * (1 + ntm) + 4 +
+                            8 * 4 * (2 * mtk + mtn) * ntm;
   GtScratch *s = new GtScratch();
   L->gt = s;
   s->Fc = (int)std::max<int64_t>(1, std::min<int64_t>(g.F, (2ll << 30) / per_field));
+  s->mq = (int)mp;
   const int64_t Fc = s->Fc;
   LCAE_CK(dmalloc(L, &s->Xp, Fc * n * mp * 2));
   LCAE_CK(dmalloc(L, &s->H16, Fc * k * mp * 2));
   LCAE_CK(dmalloc(L, &s->d16, Fc * n * mp * 2));
   LCAE_CK(dmalloc(L, &s->D16, Fc * k * mp * 2));
   LCAE_CK(dmalloc(L, &s->U, Fc * k * mp * 4));
-  LCAE_CK(dmalloc(L, &s->Q, Fc * k * mp * 4));
-  LCAE_CK(dmalloc(L, &s->G, Fc * k * mp * 4));
-  LCAE_CK(dmalloc(L, &s->R, Fc * n * mp * 4));
   LCAE_CK(dmalloc(L, &s->dXp, Fc * n * mp * 4));
   LCAE_CK(cudaMemset(s->dXp, 0, Fc * n * mp * 4));   // padded sample columns are never written: keep them zero
-  LCAE_CK(dmalloc(L, &s->dW, Fc * k * na * 4));
   LCAE_CK(dmalloc(L, &s->da, Fc * 4));
   LCAE_CK(dmalloc(L, &s->db, Fc * n * 4));
+  s->npart[0] = mtk * ntm * 4;   // GEMM 1 (U, pooling)
+  s->npart[1] = mtn * ntm * 4;   // GEMM 2 (residual)
+  s->npart[2] = mtk * ntm * 4;   // GEMM 3 (D, dalpha)
+  for (int i = 0; i < 3; ++i) LCAE_CK(dmalloc(L, &s->part[i], Fc * s->npart[i] * sizeof(double)));
+  s->nt2 = ntm;
+  LCAE_CK(dmalloc(L, &s->dbp, Fc * ntm * n * 4));
+  s->nt4 = cdiv(g.n, bnn);
+  LCAE_CK(dmalloc(L, &s->rsqp, Fc * s->nt4 * k * 4));
   // bf16 shadow of W, [F][k][n_al] (pad columns zero)
   cudaFree(L->Wb);
   L->Wb = nullptr;
   LCAE_CK(dmalloc(L, &L->Wb, (size_t)g.F * k * na * 2));
   LCAE_CK(cudaMemset(L->Wb, 0, (size_t)g.F * k * na * 2));
   // operand maps: [batch][rows][cols] with the sample (or n) extent the true size, so ragged tails load as zeros
-  const int bnm = gt::pick_bn(g.m), bnn = gt::pick_bn(g.n);
   CUtensorMap mWk, mWmn, mXmn, mXk, mHmn, mHk, mdmn, mdk, mDk, mDmn;
   bool ok = make_tmap_3d_bf16(&mWk, L->Wb, g.F, k, n, na, k * na, gt::BM) &&
             make_tmap_3d_bf16(&mWmn, L->Wb, g.F, k, n, na, k * na, gt::BK) &&
@@ -407,73 +587,95 @@ lcae_status gt_alloc(lcae_layer *L) {
             make_tmap_3d_bf16(&mdk, s->d16, Fc, n, g.m, mp, n * mp, bnn) &&
             make_tmap_3d_bf16(&mDk, s->D16, Fc, k, g.m, mp, k * mp, gt::BM) &&
             make_tmap_3d_bf16(&mDmn, s->D16, Fc, k, g.m, mp, k * mp, gt::BK);
+  // epilogue store maps (box 32 rows; fp32 32 columns, bf16 64 columns)
+  CUtensorMap sU, sH, sd, sD, sdW, sWb, sdX;
+  ok = ok && make_tmap_3d_f32(&sU, s->U, Fc, k, g.m, mp, k * mp, 32) &&
+       make_tmap_3d_bf16(&sH, s->H16, Fc, k, g.m, mp, k * mp, 32) &&
+       make_tmap_3d_bf16(&sd, s->d16, Fc, n, g.m, mp, n * mp, 32) &&
+       make_tmap_3d_bf16(&sD, s->D16, Fc, k, g.m, mp, k * mp, 32) &&
+       make_tmap_3d_f32(&sdW, L->W, g.F, k, n, L->wp, k * L->wp, 32) &&      // SGD: W~ master
+       make_tmap_3d_bf16(&sWb, L->Wb, g.F, k, n, na, k * na, 32) &&           // SGD: bf16 shadow
+       make_tmap_3d_f32(&sdX, s->dXp, Fc, n, g.m, mp, n * mp, 32);
   if (!ok) { set_error("gt path: cuTensorMapEncodeTiled failed"); return LCAE_ERR_CUDA; }
-  (void)bnm;
   auto args = [&](const CUtensorMap &A, const CUtensorMap &B, int M, int N, int K, float *C, int64_t cbs, int64_t crs) {
     gt::GemmArgs a{};
     a.tmA[0] = A; a.tmB[0] = B; a.nseg = 1; a.M = M; a.N = N; a.K = K; a.C = C; a.cbs = cbs; a.crs = crs;
+    a.g = g.g; a.gr = g.gr; a.gc = g.gc; a.lam = L->cfg.lambda_; a.eps = L->cfg.eps;
+    a.alpha = L->alpha; a.bvec = L->b; a.sigma = L->sigma; a.flags = L->flags_dev;
+    a.lr = L->cfg.lr; a.mu = L->cfg.momentum;
     return a;
   };
-  s->ga[0] = args(mWk, mXmn, g.k, g.m, g.n, s->U, k * mp, mp);       // U = W X_f
-  s->ga[1] = args(mWmn, mHmn, g.n, g.m, g.k, s->R, n * mp, mp);      // R = W^T h
-  s->ga[2] = args(mWk, mdmn, g.k, g.m, g.n, s->G, k * mp, mp);       // G = W delta
-  s->ga[3] = args(mHk, mdk, g.k, g.n, g.m, s->dW, k * na, na);       // dW = h delta^T + (alpha D) X_f^T
-  s->ga[3].tmA[1] = mDk; s->ga[3].tmB[1] = mXk; s->ga[3].nseg = 2;
-  s->ga[4] = args(mWmn, mDmn, g.n, g.m, g.k, s->dXp, n * mp, mp);    // dXp = W^T (alpha D) - delta
-  s->ga[4].C0 = s->R; s->ga[4].beta = -1.f;
+  // 1: U = W X_f; epilogue h = alpha U -> bf16, pooling, p, sum s
+  s->ga[0] = args(mWk, mXmn, g.k, g.m, g.n, s->U, k * mp, mp);
+  s->ga[0].O16 = s->H16; s->ga[0].part = s->part[0]; s->ga[0].tmC = sU; s->ga[0].tmO = sH;
+  // 2: r = W^T h; epilogue e = r + b - x, delta = 2e -> bf16, sum e^2, db partials
+  s->ga[1] = args(mWmn, mHmn, g.n, g.m, g.k, nullptr, n * mp, mp);
+  s->ga[1].I16 = s->Xp; s->ga[1].O16 = s->d16; s->ga[1].part = s->part[1]; s->ga[1].dbp = s->dbp; s->ga[1].tmO = sd;
+  // 3: G = W delta; epilogue D = G + lambda h / s, alpha D -> bf16, sum D.U
+  s->ga[2] = args(mWk, mdmn, g.k, g.m, g.n, nullptr, k * mp, mp);
+  s->ga[2].U = s->U; s->ga[2].O16 = s->D16; s->ga[2].part = s->part[2]; s->ga[2].tmO = sD;
+  // 4: sigma dW = (sigma h) delta^T + (sigma alpha D) X_f^T (two K segments into one accumulator); epilogue: projected
+  //    SGD of W~ (master + shadow), ||W~'||^2 row partials
+  s->ga[3] = args(mHk, mdk, g.k, g.n, g.m, nullptr, 0, 0);
+  s->ga[3].tmA[1] = mDk; s->ga[3].tmB[1] = mXk; s->ga[3].nseg = 2; s->ga[3].tmC = sdW; s->ga[3].tmO = sWb;
+  s->ga[3].W = L->W; s->ga[3].wp = L->wp; s->ga[3].dbp = s->rsqp; s->ga[3].vW = L->vW;
+  s->ga[3].gW = L->cfg.keep_grads ? L->gW : nullptr;
+  // 5: dXp = W^T (alpha D) - delta
+  s->ga[4] = args(mWmn, mDmn, g.n, g.m, g.k, s->dXp, n * mp, mp);
+  s->ga[4].I16 = s->d16; s->ga[4].tmC = sdX;
   return LCAE_OK;
 }
 
 void gt_free(lcae_layer *L) {
   GtScratch *s = L->gt;
   if (!s) return;
-  for (void *p : {(void *)s->Xp, (void *)s->H16, (void *)s->d16, (void *)s->D16, (void *)s->U, (void *)s->Q,
-                  (void *)s->G, (void *)s->R, (void *)s->dXp, (void *)s->dW, (void *)s->da, (void *)s->db})
+  for (void *p : {(void *)s->Xp, (void *)s->H16, (void *)s->d16, (void *)s->D16, (void *)s->U, (void *)s->dXp,
+                  (void *)s->rsqp, (void *)s->da, (void *)s->db, (void *)s->part[0], (void *)s->part[1],
+                  (void *)s->part[2], (void *)s->dbp})
     cudaFree(p);
   delete s;
   L->gt = nullptr;
 }
 
 lcae_status gt_step(lcae_layer *L, bool update, bool want_pooled, bool encode_only) {
+  using namespace gt;
   const Geo &g = L->geo;
   GtScratch &s = *L->gt;
   const int mp = L->mp;
   lcae_status st;
 #define TRY(x) do { if ((st = (x)) != LCAE_OK) return st; } while (0)
   if (update) LCAE_CK(cudaMemsetAsync(L->dxt, 0, (size_t)g.H * g.W * g.C * mp * 4, L->st));
-  Geo gp = g;
-  gp.m = mp;   // col2im over the padded sample pitch of dXp / dxt
+  s.ga[0].pooled = want_pooled ? L->pooled : nullptr;
   for (int f0 = 0; f0 < g.F; f0 += s.Fc) {
     const int Fc = std::min(s.Fc, g.F - f0);
-    for (auto &a : s.ga) a.batch = Fc;
+    for (auto &a : s.ga) { a.batch = Fc; a.f0 = f0; }
     s.ga[0].bA[0] = s.ga[1].bA[0] = s.ga[2].bA[0] = s.ga[4].bA[0] = f0;   // W maps span all fields
-    gt::gt_gather<<<Fc, 256, 0, L->st>>>(g, f0, mp, L->xt16, s.Xp);
+    gt_gather<<<Fc, 256, 0, L->st>>>(g, f0, mp, s.mq, L->xt16, s.Xp);
     LCAE_CK_LAUNCH(L);
-    TRY((gt::gemm<false, true>(L, s.ga[0])));
-    gt::gt_pool<<<Fc, 256, 0, L->st>>>(g, f0, mp, s.U, L->alpha, L->cfg.lambda_, L->cfg.eps, s.H16,
-                                       update ? s.Q : nullptr, want_pooled ? L->pooled : nullptr, L->loss_part,
-                                       encode_only ? 1 : 0);
-    LCAE_CK_LAUNCH(L);
-    if (encode_only) continue;
-    TRY((gt::gemm<true, true>(L, s.ga[1])));
-    gt::gt_resid<<<Fc, 256, 0, L->st>>>(g, f0, mp, s.R, L->b, s.Xp, s.d16, L->loss_part, s.db);
+    TRY(want_pooled ? (gemm<false, true, EPI_POOLP>(L, s.ga[0])) : (gemm<false, true, EPI_POOL>(L, s.ga[0])));
+    if (!encode_only) TRY((gemm<true, true, EPI_RESID>(L, s.ga[1])));
+    if (update) TRY((gemm<false, true, EPI_DCODE>(L, s.ga[2])));
+    gt_parts<<<Fc, 256, 0, L->st>>>(f0, g.n, L->cfg.lambda_, s.part[0], s.npart[0],
+                                    encode_only ? nullptr : s.part[1], s.npart[1], update ? s.part[2] : nullptr,
+                                    s.npart[2], s.dbp, s.nt2, L->loss_part, s.da, s.db, encode_only ? 1 : 0);
     LCAE_CK_LAUNCH(L);
     if (!update) continue;
-    TRY((gt::gemm<false, true>(L, s.ga[2])));
-    gt::gt_dcode<<<Fc, 256, 0, L->st>>>(g, f0, mp, s.G, s.Q, s.U, L->alpha, s.D16, s.da);
-    LCAE_CK_LAUNCH(L);
-    TRY((gt::gemm<false, false>(L, s.ga[3])));
-    TRY((gt::gemm<true, true>(L, s.ga[4])));
-    col2im_f32<<<L->sm_count * 8, 256, 0, L->st>>>(gp, f0, Fc, s.dXp, L->dxt);
-    LCAE_CK_LAUNCH(L);
-    if (L->cfg.keep_grads) {
-      gt::gt_copy_ab<<<256, 256, 0, L->st>>>(f0, Fc, g.n, s.da, s.db, L->galpha, L->gb);
+    TRY((gemm<true, true, EPI_SUB16>(L, s.ga[4])));   // dX first: it reads the pre-update shadow
+    s.ga[3].sb = f0;
+    if (L->vW || L->cfg.keep_grads) TRY((gemm<false, false, EPI_SGDF>(L, s.ga[3])));
+    else TRY((gemm<false, false, EPI_SGD>(L, s.ga[3])));
+    {
+      const int y0 = (f0 / g.gc) * g.s, y1 = std::min(g.H, ((f0 + Fc - 1) / g.gc) * g.s + g.rf_h);
+      gt_col2im<<<dim3(g.W, y1 - y0), 128, 0, L->st>>>(g, mp, s.mq, f0, Fc, y0, s.dXp, L->dxt);
       LCAE_CK_LAUNCH(L);
     }
-    gt::gt_update_w<<<dim3(Fc, g.k), 256, 0, L->st>>>(g, f0, L->wp, L->n_al, L->W, L->Wb, s.dW, L->vW,
-                                                      L->cfg.keep_grads ? L->gW : nullptr, L->cfg.lr, L->cfg.momentum,
-                                                      L->cfg.seed, L->step_dev, L->cfg.field_row0, L->cfg.field_col0,
-                                                      L->cfg.global_grid_c, L->reinit_dev, L->flags_dev);
+    if (L->cfg.keep_grads) {
+      gt_copy_ab<<<256, 256, 0, L->st>>>(f0, Fc, g.n, s.da, s.db, L->galpha, L->gb);
+      LCAE_CK_LAUNCH(L);
+    }
+    gt_finalize<<<Fc, 128, 0, L->st>>>(g, f0, s.nt4, s.rsqp, L->sigma, L->W, L->Wb, L->wp, L->n_al, L->vW,
+                                       L->cfg.seed, L->step_dev, L->cfg.field_row0, L->cfg.field_col0,
+                                       L->cfg.global_grid_c, L->reinit_dev, L->flags_dev);
     LCAE_CK_LAUNCH(L);
     update_ab_f32<<<256, 256, 0, L->st>>>(g, f0, Fc, L->alpha, L->b, s.da, s.db, L->va, L->vb, L->cfg.lr,
                                           L->cfg.momentum, L->cfg.alpha_min, L->flags_dev);

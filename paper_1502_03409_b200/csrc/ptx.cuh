@@ -205,6 +205,14 @@ __device__ __forceinline__ void tma_red_add_2d(const CUtensorMap *m, const void 
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
                : "memory");
 }
+// TMA tensor store: the smem box image at src -> the box at (c0, c1, c2) of the tensor (bulk_group completion;
+// elements outside the tensor are not written).
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *m, const void *src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 // Invalidate one 128-byte L2 line without writing it back (dead scratch data).
 __device__ __forceinline__ void discard_l2(const void *p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
@@ -216,6 +224,7 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t by
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // Make this thread's generic-proxy global writes visible to later async-proxy (TMA / bulk) reads.
 __device__ __forceinline__ void fence_proxy_async_global() {

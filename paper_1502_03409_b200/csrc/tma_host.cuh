@@ -51,6 +51,22 @@ inline bool make_tmap_3d_bf16(CUtensorMap *m, const void *base, uint64_t batch, 
   return r == CUDA_SUCCESS;
 }
 
+// 3D fp32 tensor [batch][rows][cols] (pitches in elements, multiples of 4); box = (32 cols, box_rows, 1), 128B
+// swizzle (the GEMM epilogue's store staging: one 128-byte row per output row).
+inline bool make_tmap_3d_f32(CUtensorMap *m, const void *base, uint64_t batch, uint64_t rows, uint64_t cols,
+                             uint64_t pitch_elems, uint64_t batch_stride_elems, uint32_t box_rows) {
+  auto fn = tma_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {cols, rows, batch};
+  cuuint64_t strides[2] = {pitch_elems * 4, batch_stride_elems * 4};
+  cuuint32_t box[3] = {32, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // 2D fp32 tensor [rows][cols] with row pitch `pitch_elems`; box = (box_cols, box_rows), no swizzle (the reduce-add
 // target of the dX staging: rows of box_cols consecutive samples).
 inline bool make_tmap_2d_f32(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols, uint64_t pitch_elems,

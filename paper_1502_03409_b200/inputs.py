@@ -76,6 +76,16 @@ CONFIGS = {
     "c3": LayerShape("c3", 200, 200, 3, 18, 18, 2, 128, 1, 256, lr=1e-3 / 256),
 }
 
+# SURVEY.md §8(d)/(f) points beyond BASELINE.json's configs (bench.py --config):
+# c15b: the paper's parameter count ("15 billion parameters") as one c3-shaped layer, 347 x 348
+#   fields of 18 x 18 x 3 -> 128 filters (15.02 B weights), batch 256, on ONE GPU;
+# c3p: the paper-exact layer 1 (16 x 16 x 3 receptive fields, stride 4 -> 4 x 4 x 24 = 384 filters;
+#   PAPER.md:111 mini-batch 192) on 300 x 300 x 3 images: 72 x 72 = 5184 fields, 1.53 B weights.
+EXTRA_CONFIGS = {
+    "c15b": LayerShape("c15b", 710, 712, 3, 18, 18, 2, 128, 1, 256, lr=1e-3 / 256),
+    "c3p": LayerShape("c3p", 300, 300, 3, 16, 16, 4, 384, 1, 192, lr=1e-3 / 192),
+}
+
 
 def round_to_bf16(a: np.ndarray) -> np.ndarray:
     """Round float32 values to the nearest bf16-representable float32 (RN-even)."""

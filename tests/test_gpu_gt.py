@@ -8,14 +8,14 @@ import numpy as np
 import pytest
 
 from oracle import lcae_oracle as O
-from paper_1502_03409_b200.inputs import LayerShape, make_images, make_params, stratified_fields
+from paper_1502_03409_b200.inputs import EXTRA_CONFIGS, LayerShape, make_images, make_params, stratified_fields
 from tests.gpu_harness import gpu_step, oracle_step
 from tests.helpers import geo_of, normwise
 from tests.test_gpu_parity import SHAPES_BF16, _compare
 
 pytestmark = pytest.mark.gpu
 
-C3P = LayerShape("c3p", 300, 300, 3, 16, 16, 4, 384, 1, 192, lr=1e-3 / 192)   # bench.py EXTRA["c3p"]
+C3P = EXTRA_CONFIGS["c3p"]
 
 GT_SHAPES = {
     # paper layer-1 field shape (16 x 16 x 3, stride 4, k = 384, m = 192) on a small image: 3 x 3 fields
@@ -173,3 +173,53 @@ def test_gt_c3p_full_size_sampled():
     print("c3p", {k: f"{v:.1e}" for k, v in errs.items()}, len(fl), "fields")
     assert all(v <= 2e-2 for v in errs.values()), errs
     assert np.abs(np.linalg.norm(W1.astype(np.float64), axis=-1) - 1).max() <= 1e-6
+
+
+@pytest.mark.parametrize("keep", [False, True])
+def test_gt_degenerate_row_reinit(keep, monkeypatch):
+    """Degenerate-row re-initialisation on the general path: the fused path's test, routed through it."""
+    from tests import test_gpu_regimes as R
+    monkeypatch.setenv("LCAE_DEV_FORCE_GT", "1")
+    R.test_degenerate_row_reinit(1, keep)
+
+
+def test_gt_alpha_clamp(monkeypatch):
+    from tests import test_gpu_regimes as R
+    monkeypatch.setenv("LCAE_DEV_FORCE_GT", "1")
+    R.test_alpha_clamp(1)
+
+
+def test_gt_nonfinite_input_is_a_data_error(monkeypatch):
+    from tests import test_gpu_regimes as R
+    monkeypatch.setenv("LCAE_DEV_FORCE_GT", "1")
+    R.test_nonfinite_input_is_a_data_error(1)
+
+
+def test_gt_trained_regime(monkeypatch):
+    """Many steps on the k = 200 shape, then one step compared with the oracle from the trained parameters (the
+    lazy projection's sigma drifts away from 1 over the steps)."""
+    import torch
+    from paper_1502_03409_b200 import lcae
+    shape = GT_SHAPES["wide-ragged"].replace(lr=1e-3 / 37)
+    W, a, b, _ = _inputs(shape)
+    L = lcae.Layer(lcae.make_config(shape, precision=lcae.BF16))
+    try:
+        L.set_params(W, a, b)
+        J0 = None
+        for t in range(150):
+            J = L.step(torch.from_numpy(make_images(shape, seed=100 + t, bf16_round=False)).cuda(), want_loss=(t % 50 == 0))
+            if t == 0:
+                J0 = J
+        L.sync()
+        Wt = np.zeros_like(W)
+        at = np.zeros_like(a)
+        bt = np.zeros_like(b)
+        L.get_params(Wt, at, bt)
+    finally:
+        L.close()
+    X = make_images(shape, seed=999, bf16_round=False)
+    out = gpu_step(shape, lcae.BF16, Wt, at, bt, X)
+    o = oracle_step(shape, Wt, at, bt, X)
+    errs = _compare(shape, 1, out, o, Wt.astype(np.float64), at.astype(np.float64), bt.astype(np.float64))
+    print("trained", J0, o["J"], {k_: f"{v:.1e}" for k_, v in errs.items()})
+    assert o["J"] < J0
