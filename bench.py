@@ -539,7 +539,8 @@ def run_paper_stack(args):
     """SURVEY.md §8(f) item 1 at the paper's geometry (R26): 300 x 300 x 3 images ->
     72 x 72 fields x 384 (1.53 B weights) -> LCN -> 69 x 69 fields x 384 over 16 x 16 x 24 windows (11.26 B) -> LCN ->
     dense 92,256 -> 4096 (0.38 B); 13.17 B parameters, mini-batch 192. k = 384 / 4096 exceed the fused bf16
-    kernel's TMEM budget (R24): every layer runs on the fp32 path. One 'step' = one greedy training step of each
+    kernel's TMEM budget (R24): in bf16 every layer runs on the general tcgen05 GEMM path (gt_path.cu), with
+    --precision fp32 on the FFMA path. One 'step' = one greedy training step of each
     layer on the same batch (layer l's input produced by the trained layers below, as in layer-wise training);
     the input chains (encode + LCN of the layers below) are timed separately."""
     import torch
@@ -547,7 +548,7 @@ def run_paper_stack(args):
     from paper_1502_03409_b200.stack import Stack, paper_stack
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     cfg = paper_stack(batch=args.batch or 192)
-    st = Stack(cfg, precision=lcae.FP32, seed=0, host_params=False)
+    st = Stack(cfg, precision=lcae.BF16 if args.prec else lcae.FP32, seed=0, host_params=False)
     pool = [torch.from_numpy(make_images(cfg.shapes[0], seed=1, index=i)).cuda() for i in range(2)]
     n = len(cfg.shapes)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -575,9 +576,20 @@ def run_paper_stack(args):
     ck = clk.summary()
     alu_peak = FP32_ALU_TFLOPS * (ck["sm_mhz"] / ck["sm_max_mhz"] if ck.get("sm_mhz") and ck.get("sm_max_mhz") else 1)
     ach = sum(flops) / (ms * 1e-3) / 1e12
+    if args.prec:   # bf16: tensor-bound; the whole three-layer step time against the bf16 peak the clocks select
+        pk = peaks()
+        burst = bool(ck.get("sm_mhz") and ck.get("sm_max_mhz") and ck["sm_mhz"] >= 0.95 * ck["sm_max_mhz"])
+        roof = {"bound": "tensor", "achieved": ach, "peak": pk["bf16"] if burst else pk["bf16_sus"],
+                "unit": "TFLOP/s", "frac": ach / (pk["bf16"] if burst else pk["bf16_sus"]), "traffic": None,
+                "kernel": "general tcgen05 path (all kernels of the three layer steps)", "kernel_ms": ms,
+                "peak_source": f"{pk['src']} {'bf16_tflops (burst)' if burst else 'bf16_tflops_sustained'}"}
+    else:
+        roof = {"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s", "frac": ach / alu_peak,
+                "traffic": None, "kernel": "fp32 path (all kernels of the three layer steps)",
+                "kernel_ms": ms, "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x SM clock"}
     line = {"metric": PAPER_METRIC, "value": cfg.shapes[0].batch / (ms * 1e-3), "unit": "images/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16" if args.prec else "f32", "data": "synthetic",
             "config": {"workload": "paper3 (PAPER.md:95 three-layer network, DESIGN.md R26)",
                        "layers": [{"name": s.name, "input": [s.img_h, s.img_w, s.img_c], "rf": s.rf_h,
                                    "stride": s.stride, "fields": s.fields, "n": s.n, "k": s.filters,
@@ -587,9 +599,7 @@ def run_paper_stack(args):
                        "params": sum(s.fields * (s.filters * s.n + s.n + 1) for s in cfg.shapes),
                        "batch": cfg.shapes[0].batch, "lcn_window": cfg.lcn_window},
             "tflops": ach,
-            "roofline": {"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s", "frac": ach / alu_peak,
-                         "traffic": None, "kernel": "fp32 path (all kernels of the three layer steps)",
-                         "kernel_ms": ms, "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x SM clock"},
+            "roofline": roof,
             "clocks": ck}
     print(json.dumps(line), flush=True)
 

@@ -551,6 +551,7 @@ lcae_status gt_alloc(lcae_layer *L) {
   GtScratch *s = new GtScratch();
   L->gt = s;
   s->Fc = (int)std::max<int64_t>(1, std::min<int64_t>(g.F, (2ll << 30) / per_field));
+  if (const char *e = getenv("LCAE_DEV_GT_FC")) s->Fc = std::max(1, std::min(s->Fc, atoi(e)));   // dev: chunk size
   s->mq = (int)mp;
   const int64_t Fc = s->Fc;
   LCAE_CK(dmalloc(L, &s->Xp, Fc * n * mp * 2));

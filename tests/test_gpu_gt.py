@@ -223,3 +223,50 @@ def test_gt_trained_regime(monkeypatch):
     errs = _compare(shape, 1, out, o, Wt.astype(np.float64), at.astype(np.float64), bt.astype(np.float64))
     print("trained", J0, o["J"], {k_: f"{v:.1e}" for k_, v in errs.items()})
     assert o["J"] < J0
+
+
+@pytest.mark.parametrize("which", ["layer2", "layer3"])
+def test_gt_paper_layer_field_shapes(which):
+    """One bf16 training step at the paper's layer-2 field shape (n = 6144, k = 384) and at the dense layer 3's full
+    shape (n = 62 * 62 * 24 = 92,256, k = 4096; one field), general path vs the oracle at 2e-2."""
+    from paper_1502_03409_b200 import lcae
+    if which == "layer2":
+        shape = LayerShape("paper2-small", 20, 20, 24, 16, 16, 4, 384, 1, 16, lam=0.1)
+    else:
+        shape = LayerShape("paper3", 62, 62, 24, 62, 62, 1, 4096, 1, 4, lam=0.01)   # m = 4: a quick fp64 oracle
+    W, a, b, X = _inputs(shape)
+    out = gpu_step(shape, lcae.BF16, W, a, b, X, forward_first=False)
+    o = oracle_step(shape, W, a, b, X)
+    errs = _compare(shape, 1, out, o, W.astype(np.float64), a.astype(np.float64), b.astype(np.float64))
+    print(which, {k_: f"{v:.1e}" for k_, v in errs.items()})
+
+
+def test_gt_paper_architecture_stack_bf16():
+    """The paper's three-layer network (R26) on a 28 x 28 image in bf16 (every layer on the
+    general path: k = 384, 384, 4096): each stage's encode against the oracle on the GPU stage's input, 2e-2."""
+    import torch
+    from paper_1502_03409_b200 import lcae
+    from paper_1502_03409_b200.stack import Stack, check_chain, paper_stack
+    from oracle.lcae_oracle import layer_gradients
+    cfg = paper_stack(batch=8, image=28, lcn_window=3)
+    check_chain(cfg)
+    X = make_images(cfg.shapes[0], seed=4, bf16_round=False)
+    st = Stack(cfg, precision=lcae.BF16, seed=0)
+    errs = {}
+    try:
+        x = torch.from_numpy(X).cuda()
+        for l, s in enumerate(cfg.shapes):
+            code = st._code(l, x)
+            W = np.zeros((s.fields, s.filters, s.n), np.float32)
+            a = np.zeros(s.fields, np.float32)
+            b = np.zeros((s.fields, s.n), np.float32)
+            st.layers[l].get_params(W, a, b)
+            want = layer_gradients(W.astype(np.float64), a.astype(np.float64), b.astype(np.float64),
+                                   x.cpu().numpy().astype(np.float64), geo_of(s))["p"]
+            errs[f"encode{l}"] = normwise(code.cpu().numpy(), want)
+            if l + 1 < len(cfg.shapes):
+                x = st.next_input(l, st._lcn(st.to_map(l, code)))
+    finally:
+        st.close()
+    print({k: f"{v:.1e}" for k, v in errs.items()})
+    assert all(v <= 2e-2 for v in errs.values()), errs
