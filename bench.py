@@ -178,22 +178,110 @@ def cpu_oracle_rate(shape, budget_s=12.0, seed=0):
     return shape.batch / t_step, done, t_used, threads
 
 
+def _oracle_worker(task):
+    """One field-parallel oracle process (BLAS threads = 1, set through the environment before numpy loads): time
+    O.step on its share of the fields. Returns (fields, seconds)."""
+    shape, fl = task
+    from oracle import lcae_oracle as O
+    if shape.name not in _X64:
+        _X64[shape.name] = make_images(shape, seed=1).astype(np.float64)
+    geo = dict(img_h=shape.img_h, img_w=shape.img_w, img_c=shape.img_c, rf_h=shape.rf_h, rf_w=shape.rf_w,
+               stride=shape.stride, pool_group=shape.pool_group, lam=shape.lam, eps=shape.eps)
+    W, a, b = make_params(shape, seed=0, fields=fl)
+    t0 = time.perf_counter()
+    O.step(W.astype(np.float64), a.astype(np.float64), b.astype(np.float64), _X64[shape.name], geo, lr=shape.lr,
+           fields=fl)
+    return len(fl), time.perf_counter() - t0
+
+
+def _blas_info():
+    try:
+        from threadpoolctl import threadpool_info
+        return ", ".join(f"{d.get('internal_api')} {d.get('version')}" for d in threadpool_info()
+                         if d.get("user_api") == "blas") or None
+    except Exception:
+        return None
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+class OraclePool:
+    """BASELINE.md §4's CPU baseline: the fp64 oracle, one process per host core (BLAS threads = 1), fields split
+    across the processes (fields are independent; each costs the same work), plus its single-core time."""
+
+    def __init__(self, shape):
+        import multiprocessing as mp
+        try:
+            self.cores = len(os.sched_getaffinity(0))
+        except Exception:
+            self.cores = os.cpu_count() or 1
+        self.procs = max(1, min(self.cores, 64))   # one oracle image batch (fp64) per process
+        self.shape = shape
+        env = {k: os.environ.get(k) for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS")}
+        for k in env:
+            os.environ[k] = "1"
+        self.pool = mp.get_context("spawn").Pool(self.procs)
+        for k, v in env.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        self.order = stratified_fields(shape, shape.fields, seed=0)
+        self.pool.map(_oracle_worker, [(shape, self.order[:1])] * self.procs)   # start-up + image generation
+        n1, t1 = self.pool.apply(_oracle_worker, ((shape, self.order[:2]),))
+        self.t_field = t1 / n1   # single-core seconds per field (BLAS threads = 1)
+
+    def sample(self, budget_s):
+        """Run a field-parallel sample sized to about budget_s of wall time; returns (images/s of the whole layer,
+        fields done, wall seconds)."""
+        per = max(1, int(budget_s / self.t_field))
+        n = min(self.shape.fields, per * self.procs)
+        fl = self.order[:n]
+        chunks = [(self.shape, fl[i::self.procs]) for i in range(self.procs) if fl[i::self.procs]]
+        t0 = time.perf_counter()
+        res = self.pool.map(_oracle_worker, chunks)
+        wall = time.perf_counter() - t0
+        done = sum(r[0] for r in res)
+        return self.shape.batch * done / (wall * self.shape.fields), done, wall
+
+    def describe(self, done, wall):
+        return {"cores": self.procs, "kind": "oracle", "single_core_value": self.shape.batch / (self.t_field * self.shape.fields),
+                "cpu_model": _cpu_model(), "blas": _blas_info(), "host_cores": self.cores,
+                "sample": f"{done} of {self.shape.fields} fields (stratified) on {self.procs} processes x 1 BLAS thread, "
+                          f"{wall:.1f} s wall, extrapolated linearly to the full layer; single_core_value: the same "
+                          f"oracle on one core"}
+
+    def close(self):
+        self.pool.terminate()
+
+
 def run_reference(args, shape):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     steps = []
-    # each step is a bounded sample of the workload; the whole --steps/--warmup run stays near 150 s
+    # each step is a bounded field-parallel sample of the workload; the whole --steps/--warmup run stays near 150 s
     per = min(args.ref_budget, max(1.0, 150.0 / (args.steps + args.warmup / 4)))
-    for _ in range(args.warmup):
-        cpu_oracle_rate(shape, budget_s=per / 4)
-    for _ in range(args.steps):
-        v, done, t_used, threads = cpu_oracle_rate(shape, budget_s=per)
-        steps.append((v, done, t_used))
+    op = OraclePool(shape)
+    try:
+        for _ in range(args.warmup):
+            op.sample(per / 4)
+        for _ in range(args.steps):
+            steps.append(op.sample(per))
+    finally:
+        op.close()
     v = statistics.median(s[0] for s in steps)
     frac = statistics.median(s[1] for s in steps) / shape.fields
-    sample = (f"{steps[0][1]} of {shape.fields} fields per step (stratified), extrapolated linearly; "
-              f"fp64 numpy oracle, {steps[0][2]:.1f} s per sample")
+    desc = op.describe(steps[0][1], steps[0][2])
     # a "step" of this arm is one bounded sample (a fraction `sample_fraction` of the layer's fields): ms_per_step is
     # its measured time, so steps x ms_per_step is the arm's wall time; value = m x fraction / sample time = the
     # images/s of the whole layer at the oracle's per-field cost (every field costs the same)
@@ -204,7 +292,7 @@ def run_reference(args, shape):
                        "rf": shape.rf_h, "stride": shape.stride, "filters": shape.filters,
                        "pool_group": shape.pool_group, "batch": shape.batch, "fields": shape.fields,
                        "sample_fraction": frac},
-            "cpu_baseline": {"value": v, "unit": "images/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "images/s", **desc},
             "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -525,10 +613,12 @@ def run_ours(args, shape):
                             "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP/FFMA x SM clock "
                                            "(median of the timed region); DESIGN.md §6"}
     if not args.no_cpu_baseline and world == 1:
-        v, done, t_used, threads = cpu_oracle_rate(shape, budget_s=args.ref_budget)
-        line["cpu_baseline"] = {"value": v, "unit": "images/s", "cores": threads, "kind": "oracle",
-                                "sample": f"{done} of {shape.fields} fields (stratified), {t_used:.1f} s, "
-                                          f"extrapolated linearly to the full layer"}
+        op = OraclePool(shape)
+        try:
+            v, done, wall = op.sample(args.ref_budget)
+        finally:
+            op.close()
+        line["cpu_baseline"] = {"value": v, "unit": "images/s", **op.describe(done, wall)}
     print(json.dumps(line), flush=True)
 
 
