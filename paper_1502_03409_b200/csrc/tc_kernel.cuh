@@ -808,6 +808,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         const int64_t wrow0 = (int64_t)f * k + qd * 32 + rr;   // W~ master row of i = 0
         // per-field invariants of this thread's E2 work, hoisted out of the tile loop
         const bool do_red = !FULL || !(P.dbg & 1), do_sgd = !FULL || !(P.dbg & 2);
+        const bool sgd_ld = !FULL || !(P.dbg & 4), sgd_st = !FULL || !(P.dbg & 8);   // dev experiments
         const bool has_v = FULL && P.vW != nullptr, keep = FULL && P.keep_grads != 0;
         const float *wrp[4];
         float sgr[4], isgr[4];
@@ -875,7 +876,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             const int cc0 = j * NT + hc + oc + 16 * h + 4 * cq;
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              wv[4 * h + i] = (rok[i] && cc0 < P.wp) ? ptx::ld_f4_ef(wrp[i] + j * NT + 16 * h, pol_ef)
+              wv[4 * h + i] = (rok[i] && cc0 < P.wp && sgd_ld) ? ptx::ld_f4_ef(wrp[i] + j * NT + 16 * h, pol_ef)
                                                      : make_float4(0, 0, 0, 0);
           }
           float4 vvp[FULL ? 4 * NCH : 1];   // momentum velocity runs, issued with the W~ runs (full variant)
@@ -1018,10 +1019,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
                   }
                   rsq4[i] = fmaf(wn[e], wn[e], rsq4[i]);
                 }
-                ptx::st_f4_ef(wp_, make_float4(wn[0], wn[1], wn[2], wn[3]), pol_ef);
-                if (cc0 < P.n_al)
-                  ptx::st_u2_ef(P.Wb + ((int64_t)f * KP + r) * P.n_al + cc0,
-                                make_uint2(ptx::pack_bf16x2(wn[0], wn[1]), ptx::pack_bf16x2(wn[2], wn[3])), pol_ef);
+                wv[4 * h + i] = make_float4(wn[0], wn[1], wn[2], wn[3]);   // stored after the second dX round
                 if (has_v) *reinterpret_cast<float4 *>(P.vW + (wp_ - P.W)) = make_float4(vo[0], vo[1], vo[2], vo[3]);
                 if (keep) {
                   const float is = isgr[i];
@@ -1031,6 +1029,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
             }
           }
           dx_round(std::integral_constant<int, 1>{}, pw1);   // second dX round (its staging read overlaps the next tile)
+          // the W~' runs (fp32 master, bf16 shadow) leave after the dX round: its shared-memory proxy fence then
+          // does not wait behind these global stores, which drain while the next tile starts
+          if (do_sgd && sgd_st) {
+#pragma unroll
+            for (int h = 0; h < NCH; ++h) {
+              const int cc0 = j * NT + hc + oc + 16 * h + 4 * cq;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                if (!rok[i] || cc0 >= P.wp) continue;
+                const int r = qd * 32 + 8 * i + rr;
+                const float4 w4 = wv[4 * h + i];
+                ptx::st_f4_ef(const_cast<float *>(wrp[i]) + j * NT + 16 * h, w4, pol_ef);
+                if (cc0 < P.n_al)
+                  ptx::st_u2_ef(P.Wb + ((int64_t)f * KP + r) * P.n_al + cc0,
+                                make_uint2(ptx::pack_bf16x2(w4.x, w4.y), ptx::pack_bf16x2(w4.z, w4.w)), pol_ef);
+              }
+            }
+          }
           TMARK(37);
         }
       }
