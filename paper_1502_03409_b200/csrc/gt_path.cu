@@ -23,8 +23,12 @@ namespace lcae {
 namespace gt {
 
 constexpr int BM = 128, BK = 64;
-constexpr int stages(int BN) { return BN >= 192 ? 3 : 4; }   // operand ring depth (shared memory: + 64 KB staging)
-constexpr int smem_bytes(int BN) { return stages(BN) * (BM * BK * 2 + BN * BK * 2) + 4 * 16384 + 1024; }
+// operand ring depth and shared memory: + per epilogue warp 16 KB of staging (SGD: 24 KB, a 4-slot W~ ring)
+constexpr int stages(int BN, bool sgd) { return sgd ? 2 : BN >= 192 ? 3 : 4; }
+constexpr int warp_stage_bytes(bool sgd) { return sgd ? 24576 : 16384; }
+constexpr int smem_bytes(int BN, bool sgd) {
+  return stages(BN, sgd) * (BM * BK * 2 + BN * BK * 2) + 4 * warp_stage_bytes(sgd) + 1024;
+}
 
 // Epilogue modes: the per-element work between the GEMMs runs on the accumulator tile while it is in registers.
 // POOLP: POOL + the pooled code p; SGD / SGDF: the projected SGD of W~ on the dW accumulator (lean / with momentum or
@@ -34,7 +38,7 @@ enum { EPI_PLAIN = 0, EPI_POOL = 1, EPI_RESID = 2, EPI_DCODE = 3, EPI_SUB16 = 4,
 struct GemmArgs {
   CUtensorMap tmA[2], tmB[2];
   int bA[2], bB[2];   // batch-coordinate offset of each operand map (W maps: the chunk's first field)
-  int nseg, M, N, K, batch;
+  int nseg, M, N, K, batch, bn;   // bn: N tile width (choose_bn)
   CUtensorMap tmC, tmO;   // store maps of C (fp32, box 32 x 32) and O16 (bf16, box 64 x 32), 128B swizzle
   float *C;           // fp32 output (PLAIN, SUB16, POOL: U)
   int64_t cbs, crs;   // C[b][i][j] at C + b cbs + i crs + j (cbs, crs multiples of 8); every per-element side
@@ -63,16 +67,18 @@ struct GemmArgs {
 // (descriptor conventions pinned by tests/test_gpu_selftest.py).
 template <bool AMN, bool BMN, int BN, int EPI>
 __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs P) {
-  constexpr int ST = stages(BN);
-  constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
-  constexpr uint32_t TCOLS = 2 * BN <= 256 ? 256 : 512;
   constexpr bool POOLING = EPI == EPI_POOL || EPI == EPI_POOLP;
   constexpr bool SGD = EPI == EPI_SGD || EPI == EPI_SGDF;
+  constexpr int ST = stages(BN, SGD);
+  constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
+  constexpr uint32_t TCOLS = 2 * BN <= 256 ? 256 : 512;
+  constexpr uint32_t WST = warp_stage_bytes(SGD), OFF16 = SGD ? 16384 : 8192;   // per-warp staging, bf16 boxes
   constexpr bool st32 = EPI == EPI_PLAIN || EPI == EPI_SUB16 || POOLING || SGD;   // fp32 output (C / W~ master)
   constexpr bool st16 = POOLING || EPI == EPI_RESID || EPI == EPI_DCODE || SGD;   // bf16 output (O16 / shadow)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[ST], empty[ST], tfull[2], tempty[2];
+  __shared__ uint64_t ringb[SGD ? 16 : 1];   // SGD: per epilogue warp, 4 W~ ring slots (TMA load complete_tx)
   __shared__ uint32_t tbase_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = cdiv(P.M, BM), nt = cdiv(P.N, BN), per = mt * nt;
@@ -80,6 +86,8 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { ptx::mbar_init(&tfull[s], 1); ptx::mbar_init(&tempty[s], 4); }
+    if (SGD)
+      for (int s = 0; s < 16; ++s) ptx::mbar_init(&ringb[s], 1);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc<TCOLS>(&tbase_s);
@@ -148,7 +156,17 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
     // through this warp's 128B-swizzled staging boxes (two fp32 32 x 32, two bf16 32 x 64: double-buffered) and
     // leave by TMA tensor stores (ragged rows / columns clipped by the tensor bounds).
     const int q = warp & 3, ew = warp - 2, sw = lane & 7;
-    uint8_t *stg = smem + ST * STAGE + ew * 16384;   // [0, 8K): fp32 boxes, [8K, 16K): bf16 boxes
+    // [0, 8K): fp32 boxes (SGD: [0, 16K) the W~ ring, read and rewritten in place), then two bf16 boxes
+    uint8_t *stg = smem + ST * STAGE + ew * WST;
+    // SGD: the W~ master box (32 rows x 32 columns) of chunk `nc` is TMA-loaded into ring slot nc % 4, two chunks
+    // ahead; the slot was last read by the store group of chunk nc - 4 (or nc - 2 when issued mid-tile)
+    auto ring_load = [&](uint32_t nc, int jj, int row0_, int bb) {
+      if constexpr (SGD) {
+        uint64_t *bar = &ringb[ew * 4 + (nc & 3)];
+        ptx::mbar_arrive_expect_tx(bar, 4096);
+        ptx::tma_load_3d(stg + (nc & 3) * 4096, &P.tmC, bar, jj, row0_, bb);
+      }
+    };
     uint32_t tc = 0, nchunk = 0, nbox = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tc) {
       const int b = tile / per, r = tile - b * per, mi = r / nt, ni = r % nt, m0 = mi * BM, n0 = ni * BN;
@@ -167,7 +185,7 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
       float dbs = 0.f;
       // per-element side input (x / delta in bf16, U or W~ in fp32), loaded one 32-column chunk ahead in registers:
       // the first chunk's loads are in flight while the accumulator is still being computed
-      constexpr bool has_in = EPI == EPI_RESID || EPI == EPI_SUB16 || EPI == EPI_DCODE || SGD;
+      constexpr bool has_in = EPI == EPI_RESID || EPI == EPI_SUB16 || EPI == EPI_DCODE;
       uint32_t raw[has_in ? 32 : 1];
       auto load_in = [&](int jj) {
         if constexpr (EPI == EPI_RESID || EPI == EPI_SUB16) {
@@ -178,7 +196,7 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
             raw[4 * h] = u.x; raw[4 * h + 1] = u.y; raw[4 * h + 2] = u.z; raw[4 * h + 3] = u.w;
           }
         } else if constexpr (has_in) {
-          const float4 *src = reinterpret_cast<const float4 *>(SGD ? P.W + wrow + jj : P.U + ro + jj);
+          const float4 *src = reinterpret_cast<const float4 *>(P.U + ro + jj);
 #pragma unroll
           for (int h = 0; h < 8; ++h) {
             const float4 u = src[h];
@@ -188,6 +206,13 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
         }
       };
       if constexpr (has_in) load_in(n0);
+      if constexpr (SGD) {
+        if (lane == 0) {
+          ptx::bulk_wait_read1();
+          ring_load(nchunk, n0, row0, P.sb + b);
+          if (32 < BN && n0 + 32 < P.N) ring_load(nchunk + 1, n0 + 32, row0, P.sb + b);
+        }
+      }
       ptx::mbar_wait(&tfull[buf], (tc >> 1) & 1);
       ptx::tc_fence_after();
 #pragma unroll 1
@@ -207,6 +232,19 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
         }
         if constexpr (has_in)
           if (c + 32 < BN && j0 + 32 < P.N) load_in(j0 + 32);
+        if constexpr (SGD) {
+          if (lane == 0) {
+            ptx::bulk_wait_read1();   // chunk nchunk - 2's store has read slot (nchunk + 2) % 4
+            if (c + 64 < BN && j0 + 64 < P.N) ring_load(nchunk + 2, j0 + 64, row0, P.sb + b);
+          }
+          ptx::mbar_wait(&ringb[ew * 4 + (nchunk & 3)], (nchunk >> 2) & 1);
+          const float *slot = reinterpret_cast<const float *>(stg + (nchunk & 3) * 4096);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 w4 = *reinterpret_cast<const float4 *>(slot + lane * 32 + 4 * (u ^ sw));
+            in[4 * u] = w4.x; in[4 * u + 1] = w4.y; in[4 * u + 2] = w4.z; in[4 * u + 3] = w4.w;
+          }
+        }
         float v[32];
         ptx::tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + buf * BN + c, v);
         ptx::tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + buf * BN + c + 16, v + 16);
@@ -307,7 +345,7 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
         if (lane == 0) ptx::bulk_wait_read1();
         __syncwarp();
         if constexpr (st32) {
-          float *sb32 = reinterpret_cast<float *>(stg + (nchunk & 1) * 4096);
+          float *sb32 = reinterpret_cast<float *>(stg + (SGD ? (nchunk & 3) : (nchunk & 1)) * 4096);
           const float *src = POOLING ? v : o;   // POOL keeps U (fp32) for GEMM 3's epilogue
 #pragma unroll
           for (int u = 0; u < 8; ++u)
@@ -317,7 +355,7 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
         const int hb = (c >> 5) & 1;   // 32-column half of the 64-column bf16 box
         const bool box_done = hb == 1 || n0 + c + 32 >= P.N;
         if constexpr (st16) {
-          uint8_t *sb16 = stg + 8192 + (nbox & 1) * 4096;
+          uint8_t *sb16 = stg + OFF16 + (nbox & 1) * 4096;
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             *reinterpret_cast<uint4 *>(sb16 + lane * 128 + 16 * ((4 * hb + u) ^ sw)) =
@@ -328,9 +366,10 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
         __syncwarp();
         if (lane == 0) {
           if (!frozen) {
-            if constexpr (st32) ptx::tma_store_3d(&P.tmC, stg + (nchunk & 1) * 4096, j0, row0, P.sb + b);
+            if constexpr (st32)
+              ptx::tma_store_3d(&P.tmC, stg + (SGD ? (nchunk & 3) : (nchunk & 1)) * 4096, j0, row0, P.sb + b);
             if constexpr (st16)
-              if (box_done) ptx::tma_store_3d(&P.tmO, stg + 8192 + (nbox & 1) * 4096, j0 - 32 * hb, row0, P.sb + b);
+              if (box_done) ptx::tma_store_3d(&P.tmO, stg + OFF16 + (nbox & 1) * 4096, j0 - 32 * hb, row0, P.sb + b);
           }
           ptx::bulk_commit();   // one group per chunk (possibly empty)
         }
@@ -357,7 +396,7 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
 
 template <bool AMN, bool BMN, int BN, int EPI>
 lcae_status launch_bn(lcae_layer *L, const GemmArgs &a) {
-  constexpr int smem = smem_bytes(BN);
+  constexpr int smem = smem_bytes(BN, EPI == EPI_SGD || EPI == EPI_SGDF);
   static bool attr = false;
   if (!attr) {
     LCAE_CK(cudaFuncSetAttribute(bgemm<AMN, BMN, BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -374,9 +413,20 @@ lcae_status launch_bn(lcae_layer *L, const GemmArgs &a) {
 
 inline int pick_bn(int N) { return N <= 64 ? 64 : N <= 128 ? 128 : N <= 192 ? 192 : 256; }
 
+// N tile width: the narrowest of {64, 128, 192, 256} covering N, narrowed further when a full chunk gives fewer tiles
+// than SMs (e.g. the paper's dense layer: one field, 32 M tiles) -- only with an MN-major B, whose boxes are 64
+// columns wide whatever BN is (K-major B maps are built for the chosen BN). Fixed per layer (the epilogue partial
+// sums are laid out by N tile).
+inline int choose_bn(int M, int N, int batch, bool bmn, int sms) {
+  int bn = pick_bn(N);
+  if (bmn)
+    while (bn > 64 && (int64_t)batch * cdiv(M, BM) * cdiv(N, bn) < sms) bn = bn == 256 ? 192 : bn - 64;
+  return bn;
+}
+
 template <bool AMN, bool BMN, int EPI>
 lcae_status gemm(lcae_layer *L, const GemmArgs &a) {
-  switch (pick_bn(a.N)) {
+  switch (a.bn) {
     case 64: return launch_bn<AMN, BMN, 64, EPI>(L, a);
     case 128: return launch_bn<AMN, BMN, 128, EPI>(L, a);
     case 192: return launch_bn<AMN, BMN, 192, EPI>(L, a);
@@ -396,7 +446,7 @@ __global__ void __launch_bounds__(256) gt_gather(Geo g, int f0, int mp, int mq, 
   const int64_t base = ((int64_t)r * g.s * rowstride + (int64_t)c * g.s * g.C) * mp;
   const uint4 *src = reinterpret_cast<const uint4 *>(xt16);
   uint4 *dst = reinterpret_cast<uint4 *>(Xp + (int64_t)b * g.n * mq);
-  for (int t = threadIdx.x; t < g.n * q8; t += blockDim.x) {
+  for (int t = blockIdx.y * blockDim.x + threadIdx.x; t < g.n * q8; t += gridDim.y * blockDim.x) {
     const int row = t / q8, qq = t - row * q8, ry = row / g.RW;
     const int64_t off = base + ((int64_t)ry * rowstride + (row - ry * g.RW)) * mp;
     dst[t] = qq < p8 ? src[off / 8 + qq] : make_uint4(0, 0, 0, 0);
@@ -409,7 +459,7 @@ __global__ void __launch_bounds__(256) gt_parts(int f0, int n, float lam, const 
                                                 int n2, const double *P3, int n3, const float *dbp, int nt2,
                                                 double *loss_part, float *da, float *db, int enc) {
   const int b = blockIdx.x, f = f0 + b;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && blockIdx.y == 0) {
     double s1 = 0.0;
     for (int e = 0; e < n1; ++e) s1 += P1[(int64_t)b * n1 + e];
     loss_part[2 * f + 1] = (double)lam * s1;
@@ -427,7 +477,7 @@ __global__ void __launch_bounds__(256) gt_parts(int f0, int n, float lam, const 
     }
   }
   if (P2)
-    for (int row = threadIdx.x; row < n; row += blockDim.x) {
+    for (int row = blockIdx.y * blockDim.x + threadIdx.x; row < n; row += gridDim.y * blockDim.x) {
       float acc = 0.f;
       for (int t = 0; t < nt2; ++t) acc += dbp[((int64_t)b * nt2 + t) * n + row];
       db[(int64_t)b * n + row] = acc;
@@ -448,7 +498,7 @@ __global__ void __launch_bounds__(128) gt_finalize(Geo g, int f0, int nt4, const
   const int b = blockIdx.x, f = f0 + b, k = g.k, n = g.n;
   if (threadIdx.x == 0) nbad = 0;
   __syncthreads();
-  for (int r = threadIdx.x; r < k; r += blockDim.x) {
+  for (int r = blockIdx.y * blockDim.x + threadIdx.x; r < k; r += gridDim.y * blockDim.x) {
     float rs = 0.f;
     for (int t = 0; t < nt4; ++t) rs += rsqp[((int64_t)b * nt4 + t) * k + r];
     if (!(rs >= FLT_MIN)) {   // R13: squared row norm below the smallest normal float
@@ -545,7 +595,7 @@ lcae_status gt_alloc(lcae_layer *L) {
   const int64_t k = g.k, n = g.n, mp = (g.m + 31) / 32 * 32, na = L->n_al;
   if (L->mp % 8 || L->n_al % 8) { set_error("gt path: pitches must be multiples of 8"); return LCAE_ERR_CONFIG; }
   const int bnm = gt::pick_bn(g.m), bnn = gt::pick_bn(g.n);
-  const int ntm = cdiv(g.m, bnm), mtk = cdiv(g.k, gt::BM), mtn = cdiv(g.n, gt::BM);
+  const int mtk = cdiv(g.k, gt::BM), mtn = cdiv(g.n, gt::BM), ntm = cdiv(g.m, 64);   // ntm: the most N tiles
   const int64_t per_field = n * mp * (2 + 2 + 4) + k * mp * (2 + 4 + 2) + k * 4 * (cdiv(g.n, bnn) + 1) + n * 4 * (1 + ntm) + 4 +
                             8 * 4 * (2 * mtk + mtn) * ntm;
   GtScratch *s = new GtScratch();
@@ -563,12 +613,14 @@ lcae_status gt_alloc(lcae_layer *L) {
   LCAE_CK(cudaMemset(s->dXp, 0, Fc * n * mp * 4));   // padded sample columns are never written: keep them zero
   LCAE_CK(dmalloc(L, &s->da, Fc * 4));
   LCAE_CK(dmalloc(L, &s->db, Fc * n * 4));
-  s->npart[0] = mtk * ntm * 4;   // GEMM 1 (U, pooling)
-  s->npart[1] = mtn * ntm * 4;   // GEMM 2 (residual)
-  s->npart[2] = mtk * ntm * 4;   // GEMM 3 (D, dalpha)
+  // N tile widths of the five GEMMs (fixed per layer: the epilogue partials are laid out by N tile)
+  const int bn1 = gt::choose_bn(g.k, g.m, (int)Fc, true, L->sm_count), bn2 = gt::choose_bn(g.n, g.m, (int)Fc, true, L->sm_count);
+  s->npart[0] = mtk * cdiv(g.m, bn1) * 4;   // GEMM 1 (U, pooling)
+  s->npart[1] = mtn * cdiv(g.m, bn2) * 4;   // GEMM 2 (residual)
+  s->npart[2] = mtk * cdiv(g.m, bn1) * 4;   // GEMM 3 (D, dalpha)
   for (int i = 0; i < 3; ++i) LCAE_CK(dmalloc(L, &s->part[i], Fc * s->npart[i] * sizeof(double)));
-  s->nt2 = ntm;
-  LCAE_CK(dmalloc(L, &s->dbp, Fc * ntm * n * 4));
+  s->nt2 = cdiv(g.m, bn2);
+  LCAE_CK(dmalloc(L, &s->dbp, Fc * s->nt2 * n * 4));
   s->nt4 = cdiv(g.n, bnn);
   LCAE_CK(dmalloc(L, &s->rsqp, Fc * s->nt4 * k * 4));
   // bf16 shadow of W, [F][k][n_al] (pad columns zero)
@@ -624,6 +676,10 @@ lcae_status gt_alloc(lcae_layer *L) {
   // 5: dXp = W^T (alpha D) - delta
   s->ga[4] = args(mWmn, mDmn, g.n, g.m, g.k, s->dXp, n * mp, mp);
   s->ga[4].I16 = s->d16; s->ga[4].tmC = sdX;
+  s->ga[0].bn = s->ga[2].bn = bn1;
+  s->ga[1].bn = s->ga[4].bn = bn2;
+  s->ga[3].bn = bnn;   // K-major B: its maps are built for this width
+  (void)bnm;
   return LCAE_OK;
 }
 
@@ -651,12 +707,13 @@ lcae_status gt_step(lcae_layer *L, bool update, bool want_pooled, bool encode_on
     const int Fc = std::min(s.Fc, g.F - f0);
     for (auto &a : s.ga) { a.batch = Fc; a.f0 = f0; }
     s.ga[0].bA[0] = s.ga[1].bA[0] = s.ga[2].bA[0] = s.ga[4].bA[0] = f0;   // W maps span all fields
-    gt_gather<<<Fc, 256, 0, L->st>>>(g, f0, mp, s.mq, L->xt16, s.Xp);
+    const int ysplit = std::max(1, std::min(64, 4 * L->sm_count / Fc));   // blocks per field (few-field layers)
+    gt_gather<<<dim3(Fc, ysplit), 256, 0, L->st>>>(g, f0, mp, s.mq, L->xt16, s.Xp);
     LCAE_CK_LAUNCH(L);
     TRY(want_pooled ? (gemm<false, true, EPI_POOLP>(L, s.ga[0])) : (gemm<false, true, EPI_POOL>(L, s.ga[0])));
     if (!encode_only) TRY((gemm<true, true, EPI_RESID>(L, s.ga[1])));
     if (update) TRY((gemm<false, true, EPI_DCODE>(L, s.ga[2])));
-    gt_parts<<<Fc, 256, 0, L->st>>>(f0, g.n, L->cfg.lambda_, s.part[0], s.npart[0],
+    gt_parts<<<dim3(Fc, ysplit), 256, 0, L->st>>>(f0, g.n, L->cfg.lambda_, s.part[0], s.npart[0],
                                     encode_only ? nullptr : s.part[1], s.npart[1], update ? s.part[2] : nullptr,
                                     s.npart[2], s.dbp, s.nt2, L->loss_part, s.da, s.db, encode_only ? 1 : 0);
     LCAE_CK_LAUNCH(L);
@@ -674,7 +731,7 @@ lcae_status gt_step(lcae_layer *L, bool update, bool want_pooled, bool encode_on
       gt_copy_ab<<<256, 256, 0, L->st>>>(f0, Fc, g.n, s.da, s.db, L->galpha, L->gb);
       LCAE_CK_LAUNCH(L);
     }
-    gt_finalize<<<Fc, 128, 0, L->st>>>(g, f0, s.nt4, s.rsqp, L->sigma, L->W, L->Wb, L->wp, L->n_al, L->vW,
+    gt_finalize<<<dim3(Fc, cdiv(g.k, 128)), 128, 0, L->st>>>(g, f0, s.nt4, s.rsqp, L->sigma, L->W, L->Wb, L->wp, L->n_al, L->vW,
                                        L->cfg.seed, L->step_dev, L->cfg.field_row0, L->cfg.field_col0,
                                        L->cfg.global_grid_c, L->reinit_dev, L->flags_dev);
     LCAE_CK_LAUNCH(L);

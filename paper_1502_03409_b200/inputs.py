@@ -84,6 +84,10 @@ CONFIGS = {
 EXTRA_CONFIGS = {
     "c15b": LayerShape("c15b", 710, 712, 3, 18, 18, 2, 128, 1, 256, lr=1e-3 / 256),
     "c3p": LayerShape("c3p", 300, 300, 3, 16, 16, 4, 384, 1, 192, lr=1e-3 / 192),
+    # the paper's layer 2 alone (R26): 69 x 69 fields of 16 x 16 x 24 (n = 6144) -> 384, 11.26 B weights
+    "paper2": LayerShape("paper2", 288, 288, 24, 16, 16, 4, 384, 1, 192, lam=0.1, lr=1e-3 / 192),
+    # the paper's dense layer 3 alone: one field of 62 x 62 x 24 = 92,256 inputs -> 4096 units
+    "paper3dense": LayerShape("paper3dense", 62, 62, 24, 62, 62, 1, 4096, 1, 192, lam=0.01, lr=1e-3 / 192),
 }
 
 
