@@ -148,8 +148,7 @@ lcae_status lcae_mp_fields(lcae_layer *L, int32_t *n_interior, int32_t *n_bounda
 /* Create a layer on the current CUDA device: validates cfg (as lcae_geometry), allocates parameters,
  * gradient/optimizer state and scratch, and initialises W to unit rows from a counter-based generator,
  * alpha = alpha_init, b = 0 (callers normally overwrite them with lcae_set_params).
- * *out receives the handle. Errors: CONFIG (also: a model-parallel bf16 layer beyond the fused kernel's
- * k <= 128 / m <= 256 / n <= 4096), CUDA (e.g. out of memory), ARG. */
+ * *out receives the handle. Errors: CONFIG, CUDA (e.g. out of memory), ARG. */
 lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out);
 
 /* Release everything the handle owns. NULL-safe. Synchronises the layer's stream first. */

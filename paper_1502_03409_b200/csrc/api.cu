@@ -307,12 +307,6 @@ lcae_status lcae_create(const lcae_config *cfg, lcae_layer **out) {
     CKF(cudaMemset(L->xt16, 0, mp * img * 2));   // padded batch columns stay zero
     CKF(dmalloc(L, &L->rowsq, F * k * 4));
     if (use_gt) {
-      if (cfg->world_size > 1 || cfg->nccl_id) {
-        set_error(std::string("model parallelism needs the fused bf16 kernel: ") +
-                  (tc_unsupported(g) ? tc_unsupported(g) : "LCAE_DEV_FORCE_GT set"));
-        lcae_destroy(L);
-        return LCAE_ERR_CONFIG;
-      }
       FAIL(gt_alloc(L));
     } else {
       FAIL(tc_alloc(L));

@@ -413,13 +413,13 @@ lcae_status launch_bn(lcae_layer *L, const GemmArgs &a) {
 
 inline int pick_bn(int N) { return N <= 64 ? 64 : N <= 128 ? 128 : N <= 192 ? 192 : 256; }
 
-// N tile width: the narrowest of {64, 128, 192, 256} covering N, narrowed further when a full chunk gives fewer tiles
-// than SMs (e.g. the paper's dense layer: one field, 32 M tiles) -- only with an MN-major B, whose boxes are 64
+// N tile width: the narrowest of {64, 128, 192, 256} covering N, narrowed further for single-field layers whose
+// tiles would not fill the SMs (the paper's dense layer: one field, 32 M tiles) -- only with an MN-major B, whose boxes are 64
 // columns wide whatever BN is (K-major B maps are built for the chosen BN). Fixed per layer (the epilogue partial
 // sums are laid out by N tile).
-inline int choose_bn(int M, int N, int batch, bool bmn, int sms) {
+inline int choose_bn(int M, int N, int batch, bool bmn, int sms, int F) {
   int bn = pick_bn(N);
-  if (bmn)
+  if (bmn && F <= 2)   // single-field (dense) layers only: a tiled (model-parallel) layer keeps the untiled N tiling
     while (bn > 64 && (int64_t)batch * cdiv(M, BM) * cdiv(N, bn) < sms) bn = bn == 256 ? 192 : bn - 64;
   return bn;
 }
@@ -614,7 +614,8 @@ lcae_status gt_alloc(lcae_layer *L) {
   LCAE_CK(dmalloc(L, &s->da, Fc * 4));
   LCAE_CK(dmalloc(L, &s->db, Fc * n * 4));
   // N tile widths of the five GEMMs (fixed per layer: the epilogue partials are laid out by N tile)
-  const int bn1 = gt::choose_bn(g.k, g.m, (int)Fc, true, L->sm_count), bn2 = gt::choose_bn(g.n, g.m, (int)Fc, true, L->sm_count);
+  const int bn1 = gt::choose_bn(g.k, g.m, (int)Fc, true, L->sm_count, g.F),
+            bn2 = gt::choose_bn(g.n, g.m, (int)Fc, true, L->sm_count, g.F);
   s->npart[0] = mtk * cdiv(g.m, bn1) * 4;   // GEMM 1 (U, pooling)
   s->npart[1] = mtn * cdiv(g.m, bn2) * 4;   // GEMM 2 (residual)
   s->npart[2] = mtk * cdiv(g.m, bn1) * 4;   // GEMM 3 (D, dalpha)

@@ -377,13 +377,14 @@ lcae_status mp_stage(lcae_layer *L, const float *xd) {
 // Phases of a model-parallel step (NCCL mode runs all three inside lcae_step / lcae_forward):
 //  0: (x staged by the caller) pack the halo others need; NCCL: exchange it on the comm stream and unpack as it
 //     lands; run the interior fields (bf16) concurrently;
-//  1: (test mode: unpack the halo the caller delivered) boundary fields (bf16) / all fields (fp32), finalize,
+//  1: (test mode: unpack the halo the caller delivered) boundary fields (bf16) / all fields (fp32, general bf16
+//     path), finalize,
 //     local loss; pack the dX of halo pixels for their owners;
 //  2: (NCCL: exchange dX) add the returned dX into the owned pixels; all-reduce the loss (NCCL).
 lcae_status mp_phase(lcae_layer *L, int phase, bool update, bool want_pooled) {
   MpState *M = L->mpst;
   const size_t es = elem_size(L);
-  const bool bf16 = L->cfg.precision == LCAE_BF16;
+  const bool bf16 = L->cfg.precision == LCAE_BF16 && !L->gt;   // the fused kernel (interior / boundary launches)
   lcae_status s;
   if (phase == 0) {
     if ((s = move_regions(L, M->in_send, image(L), M->in_send_buf, es, true, L->st))) return s;
@@ -403,6 +404,7 @@ lcae_status mp_phase(lcae_layer *L, int phase, bool update, bool want_pooled) {
     if (M->use_nccl) LCAE_CK(cudaStreamWaitEvent(L->st, M->ev_halo, 0));
     else if ((s = move_regions(L, M->in_recv, image(L), M->in_recv_buf, es, false, L->st))) return s;
     if (bf16) s = tc_step(L, update, want_pooled, false, M->flist + M->n_int, M->n_bnd, false, true, 0);
+    else if (L->gt) s = gt_step(L, update, want_pooled, false);   // general bf16 path: every field after the halo
     else s = f32_step(L, update, want_pooled);
     if (s) return s;
     if ((s = launch_loss_reduce(L, update))) return s;

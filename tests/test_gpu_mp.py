@@ -110,6 +110,8 @@ SHAPES = {
     "cluster2": LayerShape("cluster2", 36, 36, 3, 8, 8, 4, 32, 2, 200),
     "c3small": LayerShape("c3small", 56, 40, 3, 18, 18, 2, 128, 1, 256),
     "ragged": LayerShape("ragged", 29, 25, 2, 5, 7, 2, 24, 4, 40),
+    # k = 160 > 128: the general bf16 path (gt_path.cu) in every rank; fp32 for the fp32 runs
+    "wide160": LayerShape("wide160", 36, 36, 3, 8, 8, 4, 160, 2, 96),
 }
 
 
@@ -137,14 +139,14 @@ def test_model_parallel_equals_untiled(name, P, precision):
     print(name, P, precision, "interior/boundary", counts, "bytes", moved)
 
 
-@pytest.mark.parametrize("precision", [1, 0])
-def test_single_rank_nccl_mode_equals_plain_layer(precision):
+@pytest.mark.parametrize("precision,name", [(1, "c3small"), (0, "cluster2"), (1, "wide160")])
+def test_single_rank_nccl_mode_equals_plain_layer(precision, name):
     """world_size = 1 with an NCCL id: the NCCL communicator, the comm stream and events, the interior /
     boundary launches (interior leaves two SM pairs free) and the loss all-reduce all run on one GPU; the step
     equals the plain layer's (bitwise parameters)."""
     import torch
     from paper_1502_03409_b200 import lcae
-    shape = SHAPES["c3small"] if precision == 1 else SHAPES["cluster2"]
+    shape = SHAPES[name]   # wide160: k = 160, the general bf16 path
     W, a, b = make_params(shape, seed=0)
     X = make_images(shape, seed=1, bf16_round=False)
     J0, dx0, W0, a0, b0 = _untiled(shape, precision, W, a, b, X)
