@@ -6,11 +6,11 @@
 //   U  = sigma (.) W~ X_f           (k x m)   GEMM 1, epilogue: h = alpha U, sigma h (bf16), s_G, p, J_s partials
 //   R  = W~^T (sigma h)             (n x m)   GEMM 2, epilogue: delta = 2(R + b - x) (bf16), J_r, db partials
 //   G  = sigma (.) W~ delta         (k x m)   GEMM 3, epilogue: D = G + lambda h / s, sigma alpha D (bf16), dalpha
-//   dXp = W~^T (sigma alpha D) - delta (n x m) GEMM 5, epilogue subtracts delta -> overlap-add into dX (gt_col2im)
+//   dXp^T = (sigma alpha D)^T W~ - delta^T (m x n) GEMM 5, epilogue subtracts delta and TMA-reduce-adds into dX
 //   sigma dW = (sigma h) delta^T + (sigma alpha D) X^T (k x n) GEMM 4 (two K segments into one accumulator),
 //            epilogue: W~' = W~ - (lr / sigma^2) acc (master + bf16 shadow, TMA stores), ||W~'||^2 row partials;
 //   gt_finalize: sigma' = 1 / ||W~'||, degenerate rows; update_ab_f32: alpha, b.
-// Only U, dXp and the bf16 operands are written between the GEMMs (fixed-order partial sums, reduced per field by
+// Only U and the bf16 operands are written between the GEMMs (fixed-order partial sums, reduced per field by
 // gt_parts / gt_finalize: deterministic).
 #include "common.cuh"
 #include "ptx.cuh"
@@ -33,21 +33,23 @@ constexpr int smem_bytes(int BN, bool sgd) {
 // Epilogue modes: the per-element work between the GEMMs runs on the accumulator tile while it is in registers.
 // POOLP: POOL + the pooled code p; SGD / SGDF: the projected SGD of W~ on the dW accumulator (lean / with momentum or
 // kept gradients).
-enum { EPI_PLAIN = 0, EPI_POOL = 1, EPI_RESID = 2, EPI_DCODE = 3, EPI_SUB16 = 4, EPI_POOLP = 5, EPI_SGD = 6, EPI_SGDF = 7 };
+// DXRED: the transposed input-gradient GEMM (rows = samples, columns = patch rows): subtract delta and reduce-add into
+// the image gradient by TMA (boxes of consecutive pixel-feature rows).
+enum { EPI_PLAIN = 0, EPI_POOL = 1, EPI_RESID = 2, EPI_DCODE = 3, EPI_POOLP = 5, EPI_SGD = 6, EPI_SGDF = 7, EPI_DXRED = 8 };
 
 struct GemmArgs {
   CUtensorMap tmA[2], tmB[2];
   int bA[2], bB[2];   // batch-coordinate offset of each operand map (W maps: the chunk's first field)
   int nseg, M, N, K, batch, bn;   // bn: N tile width (choose_bn)
   CUtensorMap tmC, tmO;   // store maps of C (fp32, box 32 x 32) and O16 (bf16, box 64 x 32), 128B swizzle
-  float *C;           // fp32 output (PLAIN, SUB16, POOL: U)
+  float *C;           // fp32 output (PLAIN, POOL: U)
   int64_t cbs, crs;   // C[b][i][j] at C + b cbs + i crs + j (cbs, crs multiples of 8); every per-element side
                       // buffer below (bf16 or fp32) has this layout
   // epilogue operands
   int f0, g, gr, gc;  // chunk's first field; pooling group; field grid
   float lam, eps;
   const float *alpha, *bvec, *U;         // alpha [F], b [F][n] (RESID), U (DCODE)
-  const __nv_bfloat16 *I16;              // x (RESID) or delta (SUB16)
+  const __nv_bfloat16 *I16;              // x (RESID)
   __nv_bfloat16 *O16;                    // h (POOL), delta (RESID), alpha D (DCODE)
   float *pooled;                         // p [m][gr][gc][k/g] (POOL, nullable)
   double *part;                          // per (b, M tile, N tile, warp) partial: sum s, sum e^2, sum D.U
@@ -60,6 +62,11 @@ struct GemmArgs {
   int64_t wp;
   float lr, mu;
   const int *flags;                      // sticky error flags: set -> no parameter writes
+  // DXRED: the image gradient [H W C rows][mp samples] fp32 as TMA reduce targets with box heights 1, 2, .., 32;
+  // patch row j of field f is pixel-feature row base(f) + ry W C + (j - ry RW), ry = j / RW
+  CUtensorMap tmR[6];
+  int RW, s, Cc;
+  int64_t WC;
 };
 
 // C[b] (M x N, fp32) = sum over segments of A_s[b] (M x K) B_s[b] (K x N); A K-major ([M][K] in global) or
@@ -73,12 +80,13 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
   constexpr uint32_t TCOLS = 2 * BN <= 256 ? 256 : 512;
   constexpr uint32_t WST = warp_stage_bytes(SGD), OFF16 = SGD ? 16384 : 8192;   // per-warp staging, bf16 boxes
-  constexpr bool st32 = EPI == EPI_PLAIN || EPI == EPI_SUB16 || POOLING || SGD;   // fp32 output (C / W~ master)
+  constexpr bool st32 = EPI == EPI_PLAIN || POOLING || SGD;   // fp32 output (C / W~ master)
   constexpr bool st16 = POOLING || EPI == EPI_RESID || EPI == EPI_DCODE || SGD;   // bf16 output (O16 / shadow)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[ST], empty[ST], tfull[2], tempty[2];
-  __shared__ uint64_t ringb[SGD ? 16 : 1];   // SGD: per epilogue warp, 4 W~ ring slots (TMA load complete_tx)
+  constexpr bool RING = SGD || EPI == EPI_DXRED;
+  __shared__ uint64_t ringb[RING ? 16 : 1];   // per epilogue warp, 4 ring slots (SGD: W~ boxes, DXRED: delta boxes)
   __shared__ uint32_t tbase_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = cdiv(P.M, BM), nt = cdiv(P.N, BN), per = mt * nt;
@@ -86,7 +94,7 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { ptx::mbar_init(&tfull[s], 1); ptx::mbar_init(&tempty[s], 4); }
-    if (SGD)
+    if (RING)
       for (int s = 0; s < 16; ++s) ptx::mbar_init(&ringb[s], 1);
     ptx::fence_mbar_init();
   }
@@ -160,11 +168,16 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
     uint8_t *stg = smem + ST * STAGE + ew * WST;
     // SGD: the W~ master box (32 rows x 32 columns) of chunk `nc` is TMA-loaded into ring slot nc % 4, two chunks
     // ahead; the slot was last read by the store group of chunk nc - 4 (or nc - 2 when issued mid-tile)
+    // DXRED: the delta box (32 patch rows x 32 samples, bf16) of chunk nc goes to slot nc % 4 of [8K, 16K)
     auto ring_load = [&](uint32_t nc, int jj, int row0_, int bb) {
       if constexpr (SGD) {
         uint64_t *bar = &ringb[ew * 4 + (nc & 3)];
         ptx::mbar_arrive_expect_tx(bar, 4096);
         ptx::tma_load_3d(stg + (nc & 3) * 4096, &P.tmC, bar, jj, row0_, bb);
+      } else if constexpr (EPI == EPI_DXRED) {
+        uint64_t *bar = &ringb[ew * 4 + (nc & 3)];
+        ptx::mbar_arrive_expect_tx(bar, 2048);
+        ptx::tma_load_3d(stg + 8192 + (nc & 3) * 2048, &P.tmO, bar, row0_, jj, bb);   // (samples, patch rows)
       }
     };
     uint32_t tc = 0, nchunk = 0, nbox = 0;
@@ -185,10 +198,10 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
       float dbs = 0.f;
       // per-element side input (x / delta in bf16, U or W~ in fp32), loaded one 32-column chunk ahead in registers:
       // the first chunk's loads are in flight while the accumulator is still being computed
-      constexpr bool has_in = EPI == EPI_RESID || EPI == EPI_SUB16 || EPI == EPI_DCODE;
+      constexpr bool has_in = EPI == EPI_RESID || EPI == EPI_DCODE;
       uint32_t raw[has_in ? 32 : 1];
       auto load_in = [&](int jj) {
-        if constexpr (EPI == EPI_RESID || EPI == EPI_SUB16) {
+        if constexpr (EPI == EPI_RESID) {
           const uint4 *src = reinterpret_cast<const uint4 *>(P.I16 + ro + jj);
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
@@ -206,9 +219,11 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
         }
       };
       if constexpr (has_in) load_in(n0);
-      if constexpr (SGD) {
+      if constexpr (RING) {
+        ptx::fence_proxy_async_smem();   // this warp's earlier reads of the slots precede the TMA writes
+        __syncwarp();
         if (lane == 0) {
-          ptx::bulk_wait_read1();
+          if (SGD) ptx::bulk_wait_read1();
           ring_load(nchunk, n0, row0, P.sb + b);
           if (32 < BN && n0 + 32 < P.N) ring_load(nchunk + 1, n0 + 32, row0, P.sb + b);
         }
@@ -220,7 +235,7 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
         if (n0 + c >= P.N) break;   // warp-uniform
         const int j0 = n0 + c;
         float in[32];
-        if constexpr (EPI == EPI_RESID || EPI == EPI_SUB16) {
+        if constexpr (EPI == EPI_RESID) {
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
             in[2 * t] = __uint_as_float(raw[t] << 16);
@@ -232,6 +247,15 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
         }
         if constexpr (has_in)
           if (c + 32 < BN && j0 + 32 < P.N) load_in(j0 + 32);
+        if constexpr (EPI == EPI_DXRED) {
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && c + 64 < BN && j0 + 64 < P.N) ring_load(nchunk + 2, j0 + 64, row0, b);
+          ptx::mbar_wait(&ringb[ew * 4 + (nchunk & 3)], (nchunk >> 2) & 1);
+          const __nv_bfloat16 *slot = reinterpret_cast<const __nv_bfloat16 *>(stg + 8192 + (nchunk & 3) * 2048);
+#pragma unroll
+          for (int t = 0; t < 32; ++t) in[t] = __bfloat162float(slot[t * 32 + lane]);   // delta[j0 + t][i]
+        }
         if constexpr (SGD) {
           if (lane == 0) {
             ptx::bulk_wait_read1();   // chunk nchunk - 2's store has read slot (nchunk + 2) % 4
@@ -256,9 +280,10 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
         if constexpr (EPI == EPI_PLAIN) {
 #pragma unroll
           for (int t = 0; t < 32; ++t) o[t] = v[t];
-        } else if constexpr (EPI == EPI_SUB16) {
+        } else if constexpr (EPI == EPI_DXRED) {
+          // this thread: sample i; columns: patch rows j0 .. j0 + 31 (delta from the ring box, zero past the edges)
 #pragma unroll
-          for (int t = 0; t < 32; ++t) o[t] = v[t] - in[t];   // dXp = W^T (alpha D) - delta
+          for (int t = 0; t < 32; ++t) o[t] = v[t] - in[t];   // dXp^T = (sigma alpha D)^T W~ - delta^T
         } else if constexpr (SGD) {
           // the accumulator holds sigma dJ/dW. Lean: rownorm(sigma W~ - lr dJ/dW) = rownorm(W~ - (lr / sigma^2) acc),
           // so W~ is updated without the sigma scale and sigma' = 1 / ||W~'|| (gt_finalize); with momentum the
@@ -352,6 +377,11 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
             *reinterpret_cast<float4 *>(sb32 + lane * 32 + 4 * (u ^ sw)) =
                 make_float4(src[4 * u], src[4 * u + 1], src[4 * u + 2], src[4 * u + 3]);
         }
+        if constexpr (EPI == EPI_DXRED) {   // [32 patch rows][32 samples]: lane = sample, conflict-free rows
+          float *sbr = reinterpret_cast<float *>(stg + (nchunk & 1) * 4096);
+#pragma unroll
+          for (int t = 0; t < 32; ++t) sbr[t * 32 + lane] = o[t];
+        }
         const int hb = (c >> 5) & 1;   // 32-column half of the 64-column bf16 box
         const bool box_done = hb == 1 || n0 + c + 32 >= P.N;
         if constexpr (st16) {
@@ -371,6 +401,25 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
             if constexpr (st16)
               if (box_done) ptx::tma_store_3d(&P.tmO, stg + OFF16 + (nbox & 1) * 4096, j0 - 32 * hb, row0, P.sb + b);
           }
+          if constexpr (EPI == EPI_DXRED) {
+            if (!frozen) {
+              // the chunk's patch rows split into runs of consecutive pixel-feature rows, each into power-of-two boxes
+              const int fr = f / P.gc, fc = f - fr * P.gc;
+              const int64_t base = (int64_t)fr * P.s * P.WC + (int64_t)fc * P.s * P.Cc;
+              const int jend = min(j0 + 32, P.N);
+              for (int ja = j0; ja < jend;) {
+                const int ry = ja / P.RW, run_end = min(jend, (ry + 1) * P.RW);
+                int h = run_end - ja;
+                while (h > 0) {
+                  const int lg = min(5, 31 - __clz(h));
+                  ptx::tma_red_add_2d(&P.tmR[lg], stg + (nchunk & 1) * 4096 + (ja - j0) * 128, m0 + 32 * q,
+                                      (int)(base + (int64_t)ry * P.WC + (ja - ry * P.RW)));
+                  ja += 1 << lg;
+                  h -= 1 << lg;
+                }
+              }
+            }
+          }
           ptx::bulk_commit();   // one group per chunk (possibly empty)
         }
         if (st16 && box_done) ++nbox;
@@ -378,7 +427,7 @@ __global__ void __launch_bounds__(192, 1) bgemm(const __grid_constant__ GemmArgs
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
-      if constexpr (EPI != EPI_PLAIN && EPI != EPI_SUB16 && !SGD) {   // fixed-order partials (gt_parts sums them)
+      if constexpr (EPI != EPI_PLAIN && EPI != EPI_DXRED && !SGD) {   // fixed-order partials (gt_parts sums them)
         part = warp_sum(part);
         if (lane == 0) P.part[((int64_t)(b * mt + mi) * nt + ni) * 4 + q] = part;
       }
@@ -534,37 +583,6 @@ __global__ void __launch_bounds__(128) gt_finalize(Geo g, int f0, int nt4, const
   }
 }
 
-// Overlap-add of the chunk's dXp into dX by owner gather (deterministic; fields summed in row-major order): one block
-// per pixel (x, y) of the band of image rows the chunk's fields cover, float4 over (channel, sample), no divisions in
-// the field loop.
-__global__ void __launch_bounds__(128) gt_col2im(Geo g, int mp, int mq, int f0, int Fc, int y0, const float *dXp,
-                                                 float *dxt) {
-  const int y = y0 + blockIdx.y, x = blockIdx.x;
-  const int r_lo = y - g.rf_h + 1 <= 0 ? 0 : (y - g.rf_h + g.s) / g.s, r_hi = min(y / g.s, g.gr - 1);
-  const int c_lo = x - g.rf_w + 1 <= 0 ? 0 : (x - g.rf_w + g.s) / g.s, c_hi = min(x / g.s, g.gc - 1);
-  const int CM = g.C * mp;
-  float *dst = dxt + ((int64_t)y * g.W + x) * CM;
-  for (int e = 4 * threadIdx.x; e < CM; e += 4 * blockDim.x) {
-    const int ch = e / mp, i = e - ch * mp;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    bool any = false;
-    for (int r = r_lo; r <= r_hi; ++r)
-      for (int c = c_lo; c <= c_hi; ++c) {
-        const int f = r * g.gc + c;
-        if (f < f0 || f >= f0 + Fc) continue;
-        const int nrow = ((y - r * g.s) * g.rf_w + (x - c * g.s)) * g.C + ch;
-        const float4 v = *reinterpret_cast<const float4 *>(dXp + ((int64_t)(f - f0) * g.n + nrow) * mq + i);
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        any = true;
-      }
-    if (any) {
-      float4 o = *reinterpret_cast<float4 *>(dst + e);
-      o.x += acc.x; o.y += acc.y; o.z += acc.z; o.w += acc.w;
-      *reinterpret_cast<float4 *>(dst + e) = o;
-    }
-  }
-}
-
 __global__ void gt_copy_ab(int f0, int Fc, int n, const float *da, const float *db, float *ga, float *gb) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)Fc * n; t += (int64_t)gridDim.x * blockDim.x) {
     gb[(int64_t)f0 * n + t] = db[t];
@@ -578,7 +596,6 @@ struct GtScratch {
   int Fc = 0, mq = 0;   // fields per chunk; sample pitch of the per-field buffers (multiple of 32)
   __nv_bfloat16 *Xp = nullptr, *H16 = nullptr, *d16 = nullptr, *D16 = nullptr;   // [Fc][n|k][mp]
   float *U = nullptr;                                                           // [Fc][k][mp]
-  float *dXp = nullptr;                                                         // [Fc][n][mp]
   float *da = nullptr, *db = nullptr;                                           // [Fc], [Fc][n]
   double *part[3] = {nullptr, nullptr, nullptr};                                // epilogue partials of GEMMs 1-3
   int npart[3] = {0, 0, 0};                                                     // per field
@@ -596,7 +613,7 @@ lcae_status gt_alloc(lcae_layer *L) {
   if (L->mp % 8 || L->n_al % 8) { set_error("gt path: pitches must be multiples of 8"); return LCAE_ERR_CONFIG; }
   const int bnm = gt::pick_bn(g.m), bnn = gt::pick_bn(g.n);
   const int mtk = cdiv(g.k, gt::BM), mtn = cdiv(g.n, gt::BM), ntm = cdiv(g.m, 64);   // ntm: the most N tiles
-  const int64_t per_field = n * mp * (2 + 2 + 4) + k * mp * (2 + 4 + 2) + k * 4 * (cdiv(g.n, bnn) + 1) + n * 4 * (1 + ntm) + 4 +
+  const int64_t per_field = n * mp * (2 + 2) + k * mp * (2 + 4 + 2) + k * 4 * (cdiv(g.n, bnn) + 1) + n * 4 * (1 + ntm) + 4 +
                             8 * 4 * (2 * mtk + mtn) * ntm;
   GtScratch *s = new GtScratch();
   L->gt = s;
@@ -609,8 +626,6 @@ lcae_status gt_alloc(lcae_layer *L) {
   LCAE_CK(dmalloc(L, &s->d16, Fc * n * mp * 2));
   LCAE_CK(dmalloc(L, &s->D16, Fc * k * mp * 2));
   LCAE_CK(dmalloc(L, &s->U, Fc * k * mp * 4));
-  LCAE_CK(dmalloc(L, &s->dXp, Fc * n * mp * 4));
-  LCAE_CK(cudaMemset(s->dXp, 0, Fc * n * mp * 4));   // padded sample columns are never written: keep them zero
   LCAE_CK(dmalloc(L, &s->da, Fc * 4));
   LCAE_CK(dmalloc(L, &s->db, Fc * n * 4));
   // N tile widths of the five GEMMs (fixed per layer: the epilogue partials are laid out by N tile)
@@ -642,14 +657,13 @@ lcae_status gt_alloc(lcae_layer *L) {
             make_tmap_3d_bf16(&mDk, s->D16, Fc, k, g.m, mp, k * mp, gt::BM) &&
             make_tmap_3d_bf16(&mDmn, s->D16, Fc, k, g.m, mp, k * mp, gt::BK);
   // epilogue store maps (box 32 rows; fp32 32 columns, bf16 64 columns)
-  CUtensorMap sU, sH, sd, sD, sdW, sWb, sdX;
+  CUtensorMap sU, sH, sd, sD, sdW, sWb;
   ok = ok && make_tmap_3d_f32(&sU, s->U, Fc, k, g.m, mp, k * mp, 32) &&
        make_tmap_3d_bf16(&sH, s->H16, Fc, k, g.m, mp, k * mp, 32) &&
        make_tmap_3d_bf16(&sd, s->d16, Fc, n, g.m, mp, n * mp, 32) &&
        make_tmap_3d_bf16(&sD, s->D16, Fc, k, g.m, mp, k * mp, 32) &&
        make_tmap_3d_f32(&sdW, L->W, g.F, k, n, L->wp, k * L->wp, 32) &&      // SGD: W~ master
-       make_tmap_3d_bf16(&sWb, L->Wb, g.F, k, n, na, k * na, 32) &&           // SGD: bf16 shadow
-       make_tmap_3d_f32(&sdX, s->dXp, Fc, n, g.m, mp, n * mp, 32);
+       make_tmap_3d_bf16(&sWb, L->Wb, g.F, k, n, na, k * na, 32);            // SGD: bf16 shadow
   if (!ok) { set_error("gt path: cuTensorMapEncodeTiled failed"); return LCAE_ERR_CUDA; }
   auto args = [&](const CUtensorMap &A, const CUtensorMap &B, int M, int N, int K, float *C, int64_t cbs, int64_t crs) {
     gt::GemmArgs a{};
@@ -674,11 +688,22 @@ lcae_status gt_alloc(lcae_layer *L) {
   s->ga[3].tmA[1] = mDk; s->ga[3].tmB[1] = mXk; s->ga[3].nseg = 2; s->ga[3].tmC = sdW; s->ga[3].tmO = sWb;
   s->ga[3].W = L->W; s->ga[3].wp = L->wp; s->ga[3].dbp = s->rsqp; s->ga[3].vW = L->vW;
   s->ga[3].gW = L->cfg.keep_grads ? L->gW : nullptr;
-  // 5: dXp = W^T (alpha D) - delta
-  s->ga[4] = args(mWmn, mDmn, g.n, g.m, g.k, s->dXp, n * mp, mp);
-  s->ga[4].I16 = s->d16; s->ga[4].tmC = sdX;
+  // 5: dXp^T = (sigma alpha D)^T W~ - delta^T (rows = samples, columns = patch rows), reduce-added into dX by TMA
+  s->ga[4] = args(mDmn, mWmn, g.m, g.n, g.k, nullptr, 0, 0);
+  if (!make_tmap_3d_bf16_32x32(&s->ga[4].tmO, s->d16, Fc, n, g.m, mp, n * mp)) {
+    set_error("gt path: cuTensorMapEncodeTiled failed (delta)");
+    return LCAE_ERR_CUDA;
+  }
+  s->ga[4].RW = g.RW; s->ga[4].s = g.s; s->ga[4].Cc = g.C; s->ga[4].WC = (int64_t)g.W * g.C;
+  for (int lg = 0; lg < 6; ++lg)
+    if (!make_tmap_2d_f32(&s->ga[4].tmR[lg], L->dxt, (uint64_t)g.H * g.W * g.C, (uint64_t)g.m, (uint64_t)L->mp,
+                          1u << lg, 32)) {
+      set_error("gt path: cuTensorMapEncodeTiled failed (dX)");
+      return LCAE_ERR_CUDA;
+    }
   s->ga[0].bn = s->ga[2].bn = bn1;
-  s->ga[1].bn = s->ga[4].bn = bn2;
+  s->ga[1].bn = bn2;
+  s->ga[4].bn = gt::choose_bn(g.m, g.n, (int)Fc, true, L->sm_count, g.F);
   s->ga[3].bn = bnn;   // K-major B: its maps are built for this width
   (void)bnm;
   return LCAE_OK;
@@ -687,7 +712,7 @@ lcae_status gt_alloc(lcae_layer *L) {
 void gt_free(lcae_layer *L) {
   GtScratch *s = L->gt;
   if (!s) return;
-  for (void *p : {(void *)s->Xp, (void *)s->H16, (void *)s->d16, (void *)s->D16, (void *)s->U, (void *)s->dXp,
+  for (void *p : {(void *)s->Xp, (void *)s->H16, (void *)s->d16, (void *)s->D16, (void *)s->U,
                   (void *)s->rsqp, (void *)s->da, (void *)s->db, (void *)s->part[0], (void *)s->part[1],
                   (void *)s->part[2], (void *)s->dbp})
     cudaFree(p);
@@ -707,7 +732,7 @@ lcae_status gt_step(lcae_layer *L, bool update, bool want_pooled, bool encode_on
   for (int f0 = 0; f0 < g.F; f0 += s.Fc) {
     const int Fc = std::min(s.Fc, g.F - f0);
     for (auto &a : s.ga) { a.batch = Fc; a.f0 = f0; }
-    s.ga[0].bA[0] = s.ga[1].bA[0] = s.ga[2].bA[0] = s.ga[4].bA[0] = f0;   // W maps span all fields
+    s.ga[0].bA[0] = s.ga[1].bA[0] = s.ga[2].bA[0] = s.ga[4].bB[0] = f0;   // W maps span all fields
     const int ysplit = std::max(1, std::min(64, 4 * L->sm_count / Fc));   // blocks per field (few-field layers)
     gt_gather<<<dim3(Fc, ysplit), 256, 0, L->st>>>(g, f0, mp, s.mq, L->xt16, s.Xp);
     LCAE_CK_LAUNCH(L);
@@ -719,15 +744,11 @@ lcae_status gt_step(lcae_layer *L, bool update, bool want_pooled, bool encode_on
                                     s.npart[2], s.dbp, s.nt2, L->loss_part, s.da, s.db, encode_only ? 1 : 0);
     LCAE_CK_LAUNCH(L);
     if (!update) continue;
-    TRY((gemm<true, true, EPI_SUB16>(L, s.ga[4])));   // dX first: it reads the pre-update shadow
+    TRY((gemm<true, true, EPI_DXRED>(L, s.ga[4])));   // dX first: it reads the pre-update shadow
     s.ga[3].sb = f0;
+    s.ga[4].sb = 0;
     if (L->vW || L->cfg.keep_grads) TRY((gemm<false, false, EPI_SGDF>(L, s.ga[3])));
     else TRY((gemm<false, false, EPI_SGD>(L, s.ga[3])));
-    {
-      const int y0 = (f0 / g.gc) * g.s, y1 = std::min(g.H, ((f0 + Fc - 1) / g.gc) * g.s + g.rf_h);
-      gt_col2im<<<dim3(g.W, y1 - y0), 128, 0, L->st>>>(g, mp, s.mq, f0, Fc, y0, s.dXp, L->dxt);
-      LCAE_CK_LAUNCH(L);
-    }
     if (L->cfg.keep_grads) {
       gt_copy_ab<<<256, 256, 0, L->st>>>(f0, Fc, g.n, s.da, s.db, L->galpha, L->gb);
       LCAE_CK_LAUNCH(L);

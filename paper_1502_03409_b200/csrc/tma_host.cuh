@@ -51,6 +51,21 @@ inline bool make_tmap_3d_bf16(CUtensorMap *m, const void *base, uint64_t batch, 
   return r == CUDA_SUCCESS;
 }
 
+// 3D bf16 tensor [batch][rows][cols], box = (32 cols, 32 rows, 1), no swizzle (64-byte box rows; zero-filled edges)
+inline bool make_tmap_3d_bf16_32x32(CUtensorMap *m, const void *base, uint64_t batch, uint64_t rows, uint64_t cols,
+                                    uint64_t pitch_elems, uint64_t batch_stride_elems) {
+  auto fn = tma_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {cols, rows, batch};
+  cuuint64_t strides[2] = {pitch_elems * 2, batch_stride_elems * 2};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // 3D fp32 tensor [batch][rows][cols] (pitches in elements, multiples of 4); box = (32 cols, box_rows, 1), 128B
 // swizzle (the GEMM epilogue's store staging: one 128-byte row per output row).
 inline bool make_tmap_3d_f32(CUtensorMap *m, const void *base, uint64_t batch, uint64_t rows, uint64_t cols,
