@@ -25,14 +25,18 @@ lcae.lib.lcae_dev_check_canaries.restype = C.c_int
 lcae.lib.lcae_dev_check_canaries.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
 
 # every step-kernel variant: lean (keep_grads 0), full (keep_grads 1 / momentum), generic (forward / encode);
-# one and two CTAs per cluster; one field per CTA and (LCAE_DEV_MAX_CLUSTERS) several fields per CTA
+# one and two CTAs per cluster; one field per CTA and (LCAE_DEV_MAX_CLUSTERS) several fields per CTA; fp32; the
+# general bf16 path's GEMM epilogues
 CASES = [(CONFIGS["c1"], lcae.BF16, 1, 0.0, None), (CONFIGS["c1"], lcae.BF16, 0, 0.0, "2"),
          (LayerShape("cl2", 20, 20, 3, 8, 8, 4, 32, 2, 200), lcae.BF16, 1, 0.0, None),
          (LayerShape("cl2", 20, 20, 3, 8, 8, 4, 32, 2, 200), lcae.BF16, 0, 0.9, "2"),
          (LayerShape("c3tiny", 22, 22, 3, 18, 18, 2, 128, 1, 256), lcae.BF16, 0, 0.0, None),
          (LayerShape("c3tiny", 26, 26, 3, 18, 18, 2, 128, 1, 256), lcae.BF16, 1, 0.0, "2"),
          (LayerShape("ragged", 21, 25, 2, 5, 7, 2, 24, 4, 37), lcae.BF16, 1, 0.0, "3"),
-         (CONFIGS["c1"], lcae.FP32, 1, 0.0, None)]
+         (CONFIGS["c1"], lcae.FP32, 1, 0.0, None),
+         # the general bf16 path (k > 128): lean SGD epilogue, and SGDF with momentum
+         (LayerShape("wide", 21, 25, 2, 5, 7, 2, 200, 4, 37), lcae.BF16, 0, 0.0, None),
+         (LayerShape("c3p-small", 24, 24, 3, 16, 16, 4, 384, 1, 192), lcae.BF16, 1, 0.9, None)]
 if len(sys.argv) > 1:
     CASES = CASES[:int(sys.argv[1])]
 
