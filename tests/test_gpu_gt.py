@@ -15,8 +15,6 @@ from tests.test_gpu_parity import SHAPES_BF16, _compare
 
 pytestmark = pytest.mark.gpu
 
-C3P = EXTRA_CONFIGS["c3p"]
-
 GT_SHAPES = {
     # paper layer-1 field shape (16 x 16 x 3, stride 4, k = 384, m = 192) on a small image: 3 x 3 fields
     "c3p-small": LayerShape("c3p-small", 24, 24, 3, 16, 16, 4, 384, 1, 192),
@@ -116,19 +114,22 @@ def test_gt_encode_matches_forward():
     assert normwise(p2.cpu().numpy(), o["p"]) <= 2e-2
 
 
-def test_gt_c3p_full_size_sampled():
-    """c3' at full size (300 x 300 x 3, 16 x 16 x 3 fields at stride 4 -> 72 x 72 fields, k = 384,
-    m = 192; 1.53 B weights) in the launch configuration bench.py times: per-field losses, the W / alpha / b
-    updates of sampled fields and dX at a probe pixel against the oracle."""
+@pytest.mark.parametrize("name", ["c3p", "paper2"])
+def test_gt_full_size_sampled(name):
+    """Full-size layers on the general path in the launch configuration bench.py times: c3' (SURVEY.md §8(d):
+    300 x 300 x 3, 16 x 16 x 3 fields at stride 4 -> 72 x 72 fields, k = 384, m = 192; 1.53 B weights) and the
+    paper's layer 2 (R26: 288 x 288 x 24, 16 x 16 x 24 windows -> 69 x 69 fields, n = 6144, k = 384; 11.26 B
+    weights): per-field losses, the W / alpha / b updates of sampled fields and dX at a probe pixel against the
+    oracle."""
     import ctypes
     import torch
     from paper_1502_03409_b200 import lcae
-    shape = C3P
+    shape = EXTRA_CONFIGS[name]
     probe = (150, 141)
     s = shape.stride
     cover = [r * shape.grid_c + c for r in range(shape.grid_r) for c in range(shape.grid_c)
              if r * s <= probe[0] < r * s + shape.rf_h and c * s <= probe[1] < c * s + shape.rf_w]
-    fl = sorted(set(stratified_fields(shape, 8, seed=3)) | set(cover))
+    fl = sorted(set(stratified_fields(shape, 8 if name == "c3p" else 4, seed=3)) | set(cover))
     X = make_images(shape, seed=5, bf16_round=False)
     L = lcae.Layer(lcae.make_config(shape, precision=lcae.BF16, seed=7))
     try:
@@ -170,7 +171,7 @@ def test_gt_c3p_full_size_sampled():
             "alpha_update": normwise(a1.astype(np.float64) - a0, o["alpha_new"] - a0),
             "b_update": normwise(b1.astype(np.float64) - b0, o["b_new"] - b0),
             "dX_probe": normwise(row, o["dX"][:, probe[0], probe[1], :])}
-    print("c3p", {k: f"{v:.1e}" for k, v in errs.items()}, len(fl), "fields")
+    print(name, {k: f"{v:.1e}" for k, v in errs.items()}, len(fl), "fields")
     assert all(v <= 2e-2 for v in errs.values()), errs
     assert np.abs(np.linalg.norm(W1.astype(np.float64), axis=-1) - 1).max() <= 1e-6
 
