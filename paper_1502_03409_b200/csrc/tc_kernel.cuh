@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
   const uint32_t crank = CB > 1 ? ptx::cluster_ctarank() : 0;
   const int cid = blockIdx.x / CB, ncl = gridDim.x / CB;
   const int s0 = (int)crank * MC;   // first sample of this CTA
-  const int T = P.T, n = g.n, k = g.k, m = g.m, mp = P.mp;
+  const int T = P.T, n = g.n, k = g.k, m = g.m;
   // FL bit 2: generic variant (forward / encode / step chosen at run time, pooled output); otherwise the
   // kernel is the training step and the forward-only paths are compiled out
   constexpr bool TR = (FL & 1) != 0, FULL = (FL & 2) != 0, GEN = (FL & 4) != 0;
@@ -821,7 +821,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
           sgr[i] = S.sig[r];
           isgr[i] = S.isig[r];
         }
-#pragma unroll 1
         // dX piece words of the warp's two 16-column rounds, loaded one tile ahead (an L2 round trip: the 227 KB
         // shared-memory carve-out leaves L1 too small to keep the table resident)
         auto piece_words = [&](int jj, uint32_t &a0, uint32_t &a1) {
@@ -989,10 +988,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 if (!rok[i] || cc0 >= P.wp) continue;
-                const int r = qd * 32 + 8 * i + rr;
                 float *wp_ = const_cast<float *>(wrp[i]) + j * NT + 16 * h;   // = W~ + row * wp + cc0
                 LCAE_DCHECK(wp_ >= P.W && wp_ + 4 <= P.W + (int64_t)g.F * k * P.wp && cc0 + 4 <= P.wp);
-                LCAE_DCHECK(((int64_t)f * KP + r) * P.n_al + cc0 + 4 <= (int64_t)g.F * KP * P.n_al || cc0 >= P.n_al);
+                LCAE_DCHECK(((int64_t)f * KP + qd * 32 + 8 * i + rr) * P.n_al + cc0 + 4 <= (int64_t)g.F * KP * P.n_al ||
+                            cc0 >= P.n_al);
                 const float d0[4] = {dq[4 * h + i].x, dq[4 * h + i].y, dq[4 * h + i].z, dq[4 * h + i].w};
                 const float wo4[4] = {wv[4 * h + i].x, wv[4 * h + i].y, wv[4 * h + i].z, wv[4 * h + i].w};
                 float d[4], wn[4], vo[4] = {0.f, 0.f, 0.f, 0.f};
