@@ -178,6 +178,16 @@ def cpu_oracle_rate(shape, budget_s=12.0, seed=0):
     return shape.batch / t_step, done, t_used, threads
 
 
+def _oracle_init(shape):
+    """Pool initializer: every worker builds the oracle's fp64 image batch once, before any timed task."""
+    _X64[shape.name] = make_images(shape, seed=1).astype(np.float64)
+
+
+def _oracle_ready(_):
+    time.sleep(0.5)   # spreads one task per worker: all initializers have run when these return
+    return os.getpid()
+
+
 def _oracle_worker(task):
     """One field-parallel oracle process (BLAS threads = 1, set through the environment before numpy loads): time
     O.step on its share of the fields. Returns (fields, seconds)."""
@@ -229,15 +239,16 @@ class OraclePool:
         env = {k: os.environ.get(k) for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS")}
         for k in env:
             os.environ[k] = "1"
-        self.pool = mp.get_context("spawn").Pool(self.procs)
+        self.pool = mp.get_context("spawn").Pool(self.procs, initializer=_oracle_init, initargs=(shape,))
         for k, v in env.items():
             if v is None:
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
         self.order = stratified_fields(shape, shape.fields, seed=0)
-        self.pool.map(_oracle_worker, [(shape, self.order[:1])] * self.procs)   # start-up + image generation
-        n1, t1 = self.pool.apply(_oracle_worker, ((shape, self.order[:2]),))
+        self.pool.map(_oracle_ready, range(self.procs), chunksize=1)   # start-up + image generation
+        self.pool.map(_oracle_worker, [(shape, self.order[:1])] * self.procs, chunksize=1)   # warm
+        n1, t1 = self.pool.apply(_oracle_worker, ((shape, self.order[:4]),))
         self.t_field = t1 / n1   # single-core seconds per field (BLAS threads = 1)
 
     def sample(self, budget_s):
@@ -248,7 +259,7 @@ class OraclePool:
         fl = self.order[:n]
         chunks = [(self.shape, fl[i::self.procs]) for i in range(self.procs) if fl[i::self.procs]]
         t0 = time.perf_counter()
-        res = self.pool.map(_oracle_worker, chunks)
+        res = self.pool.map(_oracle_worker, chunks, chunksize=1)
         wall = time.perf_counter() - t0
         done = sum(r[0] for r in res)
         return self.shape.batch * done / (wall * self.shape.fields), done, wall
