@@ -354,12 +354,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       const int pixbase = (fr * g.s * g.W + fc * g.s) * g.C;
       // X_j = runs of consecutive image rows (one per receptive-field row): a few TMA boxes per 64-sample half;
       // the 128B swizzle follows the absolute smem address, so boxes may land at any row of the tile.
-      auto load_tile = [&](uint8_t *dst_tile, uint64_t *bar, int j) {
-        // the whole warp reads the tile's piece table at once (one load latency, not one per piece) and every
-        // lane issues the TMA boxes of its own pieces
-        static_assert(XPMAX == 64, "two piece words per lane");
+      // the whole warp reads a tile's piece table at once (one load latency, not one per piece), one tile ahead
+      // of its TMA issue, and every lane issues the boxes of its own pieces
+      static_assert(XPMAX == 64, "two piece words per lane");
+      auto piece_x = [&](int j, uint32_t &a0, uint32_t &a1) {
         const uint32_t *pc = P.xpieces + j * XPMAX;
-        const uint32_t w0 = __ldg(pc + lane), w1 = __ldg(pc + 32 + lane);
+        a0 = __ldg(pc + lane);
+        a1 = __ldg(pc + 32 + lane);
+      };
+      auto load_tile = [&](uint8_t *dst_tile, uint64_t *bar, int j, uint32_t w0, uint32_t w1) {
         if (lane == 0) ptx::mbar_arrive_expect_tx(bar, (uint32_t)min(NT, n - j * NT) * 128u * 2u);
         __syncwarp();
 #pragma unroll
@@ -377,18 +380,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
       };
       // pass 0 ring borrows the D'/delta/X/H' buffers: wait until the previous field is done with them
       if (step) TWAIT(28, ptx::mbar_wait(&S.p0_ok, (nf & 1) ^ 1));
+      uint32_t xa0, xa1, xb0 = 0, xb1 = 0;
+      piece_x(0, xa0, xa1);
       for (int j = 0; j < T; ++j, ++q0) {
         const int s = q0 % NP0;
+        if (j + 1 < T) piece_x(j + 1, xb0, xb1);
         TWAIT(29, ptx::mbar_wait(&S.p0empty[s], ((q0 / NP0) & 1) ^ 1));
-        load_tile(p0slot(S, s), &S.p0full[s], j);
+        load_tile(p0slot(S, s), &S.p0full[s], j, xa0, xa1);
+        xa0 = xb0; xa1 = xb1;
       }
       if (enc) continue;   // encode-only: the pass-0 ring's own barriers order the next field's loads
       // pass 1 ring lives in the D' buffer once the encode MMAs are done
       TWAIT(30, ptx::mbar_wait(&S.u_full, nf & 1));
+      piece_x(0, xa0, xa1);
       for (int j = 0; j < T; ++j, ++q1) {
         const uint32_t s = q1 % np1;
+        if (j + 1 < T) piece_x(j + 1, xb0, xb1);
         TWAIT(30, ptx::mbar_wait(&S.p1empty[s], ((q1 / np1) & 1) ^ 1));
-        load_tile(p1slot(S, s), &S.p1full[s], j);
+        load_tile(p1slot(S, s), &S.p1full[s], j, xa0, xa1);
+        xa0 = xb0; xa1 = xb1;
       }
       if (!step) {   // forward: the next field's pass 0 reuses D'; wait until both slots were consumed
         for (uint32_t qq = q1 - std::min<uint32_t>(q1, np1); qq < q1; ++qq)
@@ -407,8 +417,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         for (int l4 = 0; l4 < 4; ++l4) ptx::discard_l2(dsrc + (size_t)jj * 16384 + (size_t)(l4 * 32 + lane) * 128);
         ptx::fence_proxy_async_global();   // ordered before the (async-proxy) bulk stores that rewrite the lines
       };
+      piece_x(0, xa0, xa1);
       for (int j = 0; j < T; ++j, ++qx, ++qd2) {
         const int sd = qd2 & 1;
+        if (j + 1 < T) piece_x(j + 1, xb0, xb1);
         TWAIT(31, ptx::mbar_wait(&S.d2empty[sd], ((qd2 >> 1) & 1) ^ 1));
         if (j >= 2) discard_tile(j - 2);
         if (lane == 0) {
@@ -418,7 +430,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) step_kernel(const __grid_constant
         __syncwarp();
         const int s = qx % NX;
         TWAIT(31, ptx::mbar_wait(&S.xempty[s], ((qx / NX) & 1) ^ 1));
-        load_tile(S.Xr[s], &S.xfull[s], j);
+        load_tile(S.Xr[s], &S.xfull[s], j, xa0, xa1);
+        xa0 = xb0; xa1 = xb1;
       }
       for (int j = std::max(0, T - 2); j < T; ++j) {   // the field's last two reloads: wait for their MMAs
         const uint32_t qq = qd2 - T + j;
