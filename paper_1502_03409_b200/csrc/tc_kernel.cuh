@@ -161,6 +161,7 @@ __device__ __forceinline__ float residual32(float (&rv)[32], int c0, int n, cons
   const float4 *b4 = reinterpret_cast<const float4 *>(b2 + c0);   // c0 % 32 == 0: 16-byte aligned broadcasts
   const float bs = b2_ready ? 1.f : 2.f;
   if (svalid && c0 + 32 <= n && b16) {   // full run (all but the ragged last tile): no masking
+    float ja[4] = {0.f, 0.f, 0.f, 0.f};   // four accumulators: a chain of 8 FFMAs instead of 32
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const float4 bv = b4[q];
@@ -168,11 +169,11 @@ __device__ __forceinline__ float residual32(float (&rv)[32], int c0, int n, cons
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const float d = fmaf(2.f, rv[4 * q + t], bb[t]);
-        jr = fmaf(d, d, jr);
+        ja[t] = fmaf(d, d, ja[t]);
         rv[4 * q + t] = d;
       }
     }
-    return jr;
+    return (ja[0] + ja[1]) + (ja[2] + ja[3]);
   }
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
